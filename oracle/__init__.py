@@ -1,0 +1,312 @@
+"""CPU oracle for the low-rank IgA hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline leg and
+``--impl reference``) may import this package.  The product package
+``paper_1811_06797_b200`` never imports it, and it never imports the product.  The only
+shared module is ``synth`` (seeded input definitions, no method arithmetic).
+
+What it computes (each function cites the passage it follows):
+
+* ``gauss_legendre``      nq-point Gauss-Legendre rule on [-1,1] (reading G1/G2).
+* ``basis_all``           all B-spline values / first derivatives, Cox-de Boor,
+                          PAPER.md:58-63 (§2).
+* ``gram_1d``             univariate weighted Gram int beta_i^(a) beta_j^(b) w,
+                          Eq. (massMatrix1D) PAPER.md:192-196 and K^{(d)}_{k,l} PAPER.md:217-220.
+* ``assemble_csr``        full 3D matrices M (Eq. massMatrix) and
+                          K = S (Eq. stiffnessMatrix) by tensor Gauss quadrature.
+* ``apply_matfree``       the same bilinear forms applied element by element.
+* ``apply_rows``          the same bilinear forms for selected output rows.
+* ``kkt_apply``           Eq. (KKTSystem) PAPER.md:313-319 written as the paper's three
+                          gradient rows PAPER.md:306-308 per time step.
+
+Parity pins: tests/test_oracle_pins.py (P1-P12 of SURVEY.md §8(c)).
+Every function here is pinned; none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+TERM_WIDTH = 10
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (plain gcc, -O2, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp.%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-Wall",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        lib = ctypes.CDLL(_LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        I = ctypes.POINTER(ctypes.c_int)
+        I64 = ctypes.POINTER(ctypes.c_int64)
+        I32 = ctypes.POINTER(ctypes.c_int32)
+        lib.orc_gauss_legendre.argtypes = [ctypes.c_int, D, D]
+        lib.orc_basis_all.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_double, D, D]
+        lib.orc_gram_1d.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int, D]
+        lib.orc_quad_nodes.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_int, D, I64]
+        lib.orc_csr_nnz.argtypes = [I, I, ctypes.c_int]
+        lib.orc_csr_nnz.restype = ctypes.c_int64
+        common = [I, I, D, D, D, ctypes.c_int, ctypes.c_int, D, I, D, ctypes.c_int]
+        lib.orc_assemble_csr.argtypes = common + [I64, I32, D, D]
+        lib.orc_spmv.argtypes = [ctypes.c_int64, I64, I32, D, D, D]
+        lib.orc_apply_matfree.argtypes = common + [D, D, D]
+        lib.orc_apply_rows.argtypes = common + [D, ctypes.c_int64, I64, D, D]
+        _lib = lib
+    return _lib
+
+
+def _dp(a: Optional[np.ndarray]):
+    if a is None:
+        return ctypes.POINTER(ctypes.c_double)()
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+# ----------------------------------------------------------------------------------- 1D
+def gauss_legendre(m: int) -> Tuple[np.ndarray, np.ndarray]:
+    x = np.zeros(m)
+    w = np.zeros(m)
+    if _L().orc_gauss_legendre(m, _dp(x), _dp(w)):
+        raise ValueError("bad m")
+    return x, w
+
+
+def basis_all(knots, p: int, t: float) -> Tuple[np.ndarray, np.ndarray]:
+    k = np.ascontiguousarray(knots, dtype=np.float64)
+    n = len(k) - p - 1
+    v = np.zeros(n)
+    d = np.zeros(n)
+    if _L().orc_basis_all(_dp(k), n, p, float(t), _dp(v), _dp(d)):
+        raise ValueError("bad knot vector")
+    return v, d
+
+
+def quad_nodes(knots, p: int, nq: int) -> np.ndarray:
+    k = np.ascontiguousarray(knots, dtype=np.float64)
+    n = len(k) - p - 1
+    cnt = ctypes.c_int64(0)
+    if _L().orc_quad_nodes(_dp(k), n, p, nq, None, ctypes.byref(cnt)):
+        raise ValueError("bad knot vector")
+    out = np.zeros(cnt.value)
+    _L().orc_quad_nodes(_dp(k), n, p, nq, _dp(out), ctypes.byref(cnt))
+    return out
+
+
+def gram_1d(knots, p: int, nq: int, amp: float, k: float, phi: float, a: int, b: int) -> np.ndarray:
+    """Dense n x n: G[i, j] = int beta_i^(a) beta_j^(b) (1 + amp sin(k pi t + phi)) dt."""
+    kn = np.ascontiguousarray(knots, dtype=np.float64)
+    n = len(kn) - p - 1
+    out = np.zeros((n, n))
+    if _L().orc_gram_1d(_dp(kn), n, p, nq, amp, k, phi, a, b, _dp(out)):
+        raise ValueError("bad input")
+    return out
+
+
+# ----------------------------------------------------------------------------------- 3D
+@dataclass
+class Problem:
+    """A 3D tensor-product spline space with separable closed-form weights.
+
+    knots: [kx, ky, kz]; p: degree per direction (x, y, z); nq: Gauss points per span.
+    mass_terms: [Rm, 10] term rows (synth layout) or None (no mass).
+    q_terms:    9 arrays [R_kl, 10] for q_kl (k*3+l, k,l over x,y,z), empty => zero block.
+    """
+    knots: List[np.ndarray]
+    p: Sequence[int]
+    nq: int
+    mass_terms: Optional[np.ndarray]
+    q_terms: Optional[List[np.ndarray]]
+    dirichlet: bool = False
+    _c: dict = field(default_factory=dict, repr=False)
+
+    def __post_init__(self):
+        self.knots = [np.ascontiguousarray(k, dtype=np.float64) for k in self.knots]
+        self.p = [int(v) for v in self.p]
+        n = [len(self.knots[d]) - self.p[d] - 1 for d in range(3)]
+        self._n = np.array(n, dtype=np.int32)
+        self._p = np.array(self.p, dtype=np.int32)
+        if self.mass_terms is None or len(self.mass_terms) == 0:
+            self._tm = np.zeros((1, TERM_WIDTH))
+            self._ntm = 0
+        else:
+            self._tm = np.ascontiguousarray(self.mass_terms, dtype=np.float64).reshape(-1, TERM_WIDTH)
+            self._ntm = self._tm.shape[0]
+        qs = self.q_terms if self.q_terms is not None else [np.zeros((0, TERM_WIDTH))] * 9
+        assert len(qs) == 9
+        self._ntq = np.array([0 if q is None else np.asarray(q).reshape(-1, TERM_WIDTH).shape[0] for q in qs],
+                             dtype=np.int32)
+        cat = [np.asarray(q, dtype=np.float64).reshape(-1, TERM_WIDTH) for q in qs if q is not None and len(q)]
+        self._tq = np.ascontiguousarray(np.concatenate(cat, 0)) if cat else np.zeros((1, TERM_WIDTH))
+
+    @property
+    def n(self):
+        return [int(v) for v in self._n]
+
+    @property
+    def dims(self):
+        """kept DoF extents (mx, my, mz)"""
+        return [v - 2 if self.dirichlet else v for v in self.n]
+
+    @property
+    def ndof(self) -> int:
+        mx, my, mz = self.dims
+        return mx * my * mz
+
+    def _args(self):
+        return (_ip(self._n), _ip(self._p), _dp(self.knots[0]), _dp(self.knots[1]), _dp(self.knots[2]),
+                self.nq, self._ntm, _dp(self._tm), _ip(self._ntq), _dp(self._tq), int(self.dirichlet))
+
+
+def problem_from_config(cfg, weights, n: Optional[int] = None, nq: Optional[int] = None) -> Problem:
+    """Oracle problem for a synth config (uniform open knots, reading A weights)."""
+    import synth
+    nn = cfg.n if n is None else n
+    knots = [synth.uniform_open_knots(nn, cfg.p) for _ in range(3)]
+    return Problem(knots=knots, p=[cfg.p] * 3, nq=(cfg.p + 1) if nq is None else nq,
+                   mass_terms=weights.mass, q_terms=weights.q_block_terms(), dirichlet=cfg.dirichlet)
+
+
+def assemble_csr(P: Problem, mass: bool = True, stiff: bool = True):
+    """(M, S) as scipy.sparse.csr_matrix over the kept DoFs (row-major z,y,x)."""
+    import scipy.sparse as sp
+    nnz = _L().orc_csr_nnz(_ip(P._n), _ip(P._p), int(P.dirichlet))
+    N = P.ndof
+    rowptr = np.zeros(N + 1, dtype=np.int64)
+    col = np.zeros(nnz, dtype=np.int32)
+    vm = np.zeros(nnz) if mass else None
+    vs = np.zeros(nnz) if stiff else None
+    rc = _L().orc_assemble_csr(*P._args(), rowptr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                               col.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dp(vm), _dp(vs))
+    if rc:
+        raise ValueError("oracle assembly failed")
+    M = sp.csr_matrix((vm, col, rowptr), shape=(N, N)) if mass else None
+    S = sp.csr_matrix((vs, col, rowptr), shape=(N, N)) if stiff else None
+    return M, S
+
+
+def spmv(A, x: np.ndarray) -> np.ndarray:
+    """naive CSR SpMV (row sums in column order), the oracle's y = A x."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.zeros(A.shape[0])
+    _L().orc_spmv(A.shape[0], A.indptr.astype(np.int64).ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                  A.indices.astype(np.int32).ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                  _dp(np.ascontiguousarray(A.data)), _dp(x), _dp(y))
+    return y
+
+
+def apply_matfree(P: Problem, x: np.ndarray, mass: bool = True, stiff: bool = True):
+    """(M x, S x) for x of shape [..., mz, my, mx] by the element-loop bilinear form."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    lead = x.shape[:-3]
+    xf = x.reshape(-1, P.ndof)
+    yM = np.zeros_like(xf) if mass else None
+    yS = np.zeros_like(xf) if stiff else None
+    for b in range(xf.shape[0]):
+        xb = np.ascontiguousarray(xf[b])
+        om = np.zeros(P.ndof) if mass else None
+        os_ = np.zeros(P.ndof) if stiff else None
+        if _L().orc_apply_matfree(*P._args(), _dp(xb), _dp(om), _dp(os_)):
+            raise ValueError("oracle apply failed")
+        if mass:
+            yM[b] = om
+        if stiff:
+            yS[b] = os_
+    shp = lead + tuple(x.shape[-3:])
+    return (yM.reshape(shp) if mass else None, yS.reshape(shp) if stiff else None)
+
+
+def apply_rows(P: Problem, x: np.ndarray, rows: np.ndarray, mass: bool = True, stiff: bool = True):
+    """(M x)[rows], (S x)[rows] for ONE vector x (kept-DoF linear row indices)."""
+    xb = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    assert xb.size == P.ndof
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    yM = np.zeros(rows.size) if mass else None
+    yS = np.zeros(rows.size) if stiff else None
+    if _L().orc_apply_rows(*P._args(), _dp(xb), rows.size, rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                           _dp(yM), _dp(yS)):
+        raise ValueError("oracle apply_rows failed")
+    return yM, yS
+
+
+# ----------------------------------------------------------------------------------- KKT
+def kkt_apply(applyM, applyS, X: np.ndarray, tau: float, beta: float) -> np.ndarray:
+    """Eq. (KKTSystem) PAPER.md:313-319 applied to X = [y, u, lam], each [n_t, N].
+
+    Written as the paper's gradient rows, k = 1..n_t, with
+    y_0 = 0 and lambda_{n_t+1} = 0 (reading G9: tau kept as in
+    PAPER.md:291,298,308):
+      r_y[k]   = tau M y_k - M lam_{k+1} + M lam_k + tau K lam_k
+      r_u[k]   = tau beta M u_k - tau M lam_k
+      r_lam[k] = M y_k - M y_{k-1} + tau K y_k - tau M u_k
+    applyM / applyS map one [N] vector to M v / K v (oracle routes)."""
+    y, u, lam = X[0], X[1], X[2]
+    nt = y.shape[0]
+    My = [applyM(y[k]) for k in range(nt)]
+    Mu = [applyM(u[k]) for k in range(nt)]
+    Ml = [applyM(lam[k]) for k in range(nt)]
+    Sy = [applyS(y[k]) for k in range(nt)]
+    Sl = [applyS(lam[k]) for k in range(nt)]
+    out = np.zeros_like(X)
+    for k in range(nt):
+        Ml_next = Ml[k + 1] if k + 1 < nt else 0.0
+        My_prev = My[k - 1] if k >= 1 else 0.0
+        out[0, k] = tau * My[k] - Ml_next + Ml[k] + tau * Sl[k]
+        out[1, k] = tau * beta * Mu[k] - tau * Ml[k]
+        out[2, k] = My[k] - My_prev + tau * Sy[k] - tau * Mu[k]
+    return out
+
+
+def kkt_apply_csr(M, S, X: np.ndarray, tau: float, beta: float) -> np.ndarray:
+    shp = X.shape
+    Xf = X.reshape(3, shp[1], -1)
+    out = kkt_apply(lambda v: spmv(M, v), lambda v: spmv(S, v), Xf, tau, beta)
+    return out.reshape(shp)
+
+
+def kkt_rows(P: Problem, X: np.ndarray, tau: float, beta: float, steps: Sequence[int],
+             rows: np.ndarray) -> np.ndarray:
+    """Sampled KKT outputs: out[blk, j, i] for time steps `steps` (0-based) and spatial
+    rows `rows`, via the same three paper rows with row-restricted applies."""
+    nt = X.shape[1]
+    Xf = X.reshape(3, nt, -1)
+    res = np.zeros((3, len(steps), len(rows)))
+
+    def M_(v):
+        return apply_rows(P, v, rows, mass=True, stiff=False)[0]
+
+    def S_(v):
+        return apply_rows(P, v, rows, mass=False, stiff=True)[1]
+
+    for j, k in enumerate(steps):
+        y, u, lam = Xf[0], Xf[1], Xf[2]
+        My = M_(y[k]); Mu = M_(u[k]); Ml = M_(lam[k])
+        Ml_next = M_(lam[k + 1]) if k + 1 < nt else 0.0
+        My_prev = M_(y[k - 1]) if k >= 1 else 0.0
+        Sy = S_(y[k]); Sl = S_(lam[k])
+        res[0, j] = tau * My - Ml_next + Ml + tau * Sl
+        res[1, j] = tau * beta * Mu - tau * Ml
+        res[2, j] = My - My_prev + tau * Sy - tau * Mu
+    return res
