@@ -1,0 +1,167 @@
+/*
+ * iga_lr.h — C ABI of the B200-native low-rank IgA operator library (libigalr.so).
+ *
+ * The hot path of arXiv:1811.06797 ("low-rank IgA"): mass and stiffness matrices held as
+ * sums of Kronecker products of banded univariate B-spline matrices,
+ *     M = sum_r  M_r^z (x) M_r^y (x) M_r^x                 Eq. (massFinal)
+ *     K = sum_kl sum_r K_klr^z (x) K_klr^y (x) K_klr^x     Eq. (stiffnessFinal)
+ * (the build calls K "S"), their univariate factors assembled by Gauss quadrature
+ *     M^(d)(w)_ij     = int beta_i beta_j w                 Eq. (massMatrix1D)
+ *     K^(d)_kl(q)_ij  = int delta(l,d)beta_i delta(k,d)beta_j q
+ * and the implicit-Euler KKT matvec of Eq. (KKTSystem) PAPER.md:313-319 with
+ *     calM = I (x) M,  calK = I (x) tau K + C (x) M        Eqs. (M_kron)/(K_kron) PAPER.md:316,326-331.
+ *
+ * Conventions
+ *   - Directions: index 0 = x (fastest, contiguous), 1 = y, 2 = z (slowest).  The paper's
+ *     (x)_{d=1..D} lists the slowest direction first.
+ *   - Vectors are fp64, C-ordered [batch][nz][ny][nx] in DEVICE memory unless a function
+ *     says HOST.  With IGA_DIRICHLET the extents are the interior ones (n_d - 2).
+ *   - Every function returns iga_status (0 == IGA_OK).  On failure a message is stored in a
+ *     thread-local buffer readable with iga_last_error().  No CPU fallback exists: a missing
+ *     or failing GPU returns IGA_ECUDA.
+ *   - Device work is stream-ordered on the caller's stream (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  No call synchronises the device except
+ *     iga_lr_assemble_factors (it waits for its own uploads) and the *_host entry points.
+ *   - Thread safety: an iga_lr_op is immutable after assembly; concurrent applies on
+ *     different streams are allowed (scratch memory is stream-ordered, cudaMallocAsync).
+ */
+#ifndef IGA_LR_H
+#define IGA_LR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IGA_OK = 0,
+    IGA_EINVAL = 1,        /* invalid argument (knots, sizes, pointers, aliasing, tau/beta) */
+    IGA_ENOMEM = 2,        /* host or device allocation failed */
+    IGA_ECUDA = 3,         /* CUDA runtime error (message carries cudaGetErrorString) */
+    IGA_EUNSUPPORTED = 4,  /* degree / quadrature size / plan shape outside compiled range */
+    IGA_ESTATE = 5         /* operation needs a part the op was not assembled with */
+} iga_status;
+
+/* Opaque assembled operator.  Owns its device memory (banded factors + plan). */
+typedef struct iga_lr_op iga_lr_op;
+
+/* One univariate spline space: degree p >= 1, n >= p+1 basis functions, open knot vector
+   of n+p+1 HOST doubles (Eq. (knotVector): first/last p+1 knots 0/1,
+   nondecreasing, interior multiplicity <= p).  Copied by the library. */
+typedef struct {
+    int32_t p;
+    int32_t n;
+    const double* knots;
+} iga_dir;
+
+/* Tensor-product space S^3 = S_x (x) S_y (x) S_z.  nq = Gauss points per
+   nonempty knot span in every direction (0 => p+1, reading G1 of DESIGN.md). */
+typedef struct {
+    iga_dir dir[3];
+    int32_t nq;
+} iga_space;
+
+/* A rank-R separable weight  f(x,y,z) = sum_r coef[r] * f_r^x(x) f_r^y(y) f_r^z(z)
+   (the paper's W_R : B~ of Eq. (weightLowRank), and q_kl PAPER.md:202-206).
+   tab[d] is a HOST array [R][nnodes_d]: f_r^d tabulated at the quadrature nodes of direction
+   d in the order returned by iga_quad_nodes (the caller evaluates w_r^(d).B~^(d) there).
+   coef may be NULL (all ones).  Copied by the library. */
+typedef struct {
+    int32_t R;
+    const double* coef;
+    const double* tab[3];
+} iga_sep;
+
+/* flags of iga_lr_assemble_factors */
+#define IGA_DIRICHLET 0x1u   /* drop the first and last basis index in every direction
+                                ("omitting the boundary nodes") */
+
+/* flags of the apply entry points (kernel path selection; results agree to rounding) */
+#define IGA_PATH_AUTO 0x0u      /* fused sm_100a kernel when the plan fits, else unfused */
+#define IGA_PATH_UNFUSED 0x10u  /* one launch per mode-product stage through HBM scratch */
+#define IGA_PATH_FUSED 0x20u    /* fused kernel; IGA_EUNSUPPORTED if the plan does not fit */
+
+/* Quadrature nodes of direction dir (0..2): nq-point Gauss-Legendre on each nonempty span,
+   ascending.  nodes_out may be NULL to query *nnodes (= nonempty spans * nq). HOST memory. */
+iga_status iga_quad_nodes(const iga_space* sp, int32_t dir, double* nodes_out, int64_t* nnodes);
+
+/* Assemble the banded univariate factors on the GPU and build the evaluation plan.
+     omega : mass weight (NULL => op has no mass part)                      Eq. (massFinal)
+     q     : array of 9 pointers, q[k*3+l] = weight q_kl of Eq. (stiffnessMatrix)
+             (k = direction differentiated on the column/test function j, l = on the row
+             function i: K_ij = sum_kl int q_kl d_l beta_i d_k beta_j);
+             q == NULL => no stiffness part; q[b] == NULL => zero block.
+   Univariate factors are deduplicated by (direction, tabulated weight content, derivative
+   pattern); Dirichlet slicing is applied to every factor.  Blocks on `stream` until the
+   factors are resident.  *out receives a new op (free with iga_lr_destroy). */
+iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, const iga_sep* const* q,
+                                   uint32_t flags, void* stream, iga_lr_op** out);
+
+void iga_lr_destroy(iga_lr_op* op);
+
+/* y_mass = alpha * M x   (if y_mass != NULL)
+   y_stiff = gamma * S x  (if y_stiff != NULL)
+   If y_mass == y_stiff (non-NULL) the single output receives alpha*M x + gamma*S x.
+   x, y: DEVICE fp64 [batch][nz][ny][nx], 8-byte aligned, outputs must not alias x.
+   flags: IGA_PATH_*.  Errors: IGA_EINVAL (batch < 1, NULL x, aliasing, misalignment),
+   IGA_ESTATE (output requested for a part the op lacks). */
+iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, double* y_stiff, double alpha,
+                        double gamma, int32_t batch, uint32_t flags, void* stream);
+
+/* Two-input form used by the KKT matvec: out = alpha * M x_mass + gamma * S x_stiff
+   (either input may be NULL to drop that part). Same layout rules as iga_lr_apply. */
+iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out,
+                         double alpha, double gamma, int32_t batch, uint32_t flags, void* stream);
+
+/* KKT matvec, Eq. (KKTSystem) PAPER.md:313-319:
+     out = [ tau calM, 0, calK^T ; 0, tau beta calM, -tau calM ; calK, -tau calM, 0 ] in
+   with calM = I_nt (x) M, calK = I_nt (x) tau S + C (x) M, C = bidiagonal (1 on the
+   diagonal, -1 below).  in/out: DEVICE fp64 [3][n_t][nz][ny][nx], blocks
+   (y, u, lambda).  Needs an op with mass and stiffness (else IGA_ESTATE);
+   tau > 0, beta > 0, n_t >= 1 (else IGA_EINVAL).  in and out must not alias. */
+iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in,
+                         double* out, uint32_t flags, void* stream);
+
+/* End-to-end variants with HOST buffers (pageable or pinned): copy in, apply, copy out,
+   synchronise `stream`.  Device staging is stream-ordered scratch owned by the call. */
+iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host,
+                             double* y_stiff_host, double alpha, double gamma, int32_t batch, uint32_t flags,
+                             void* stream);
+iga_status iga_kkt_apply_host(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in_host,
+                              double* out_host, uint32_t flags, void* stream);
+
+/* ---------------------------------------------------------------- introspection */
+typedef struct {
+    int64_t dims[3];             /* kept DoF extents (x, y, z) */
+    int32_t p[3];
+    int32_t nq;
+    int32_t n_factors[3];        /* distinct banded factors per direction */
+    int32_t n_rounds;            /* plan rounds (shared-prefix evaluation groups) */
+    int32_t n_xprod, n_yprod, n_zprod; /* mode products per vector in the plan */
+    int32_t has_mass, has_stiff;
+    int32_t fused_ok;            /* 1 if the fused kernel supports this plan */
+    double plan_flops_per_vec;   /* algorithmic flops of one mass+stiffness apply of one vector */
+    double min_bytes_per_vec;    /* 8 * (1 input + outputs) * N */
+} iga_lr_info_t;
+
+iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info);
+
+/* Copy factor `factor_id` of direction `dir` to HOST band storage [m_d][2p+1]:
+   band[i*(2p+1) + k] = F[i][i-p+k] (0 outside the matrix).  *pattern receives a*2+b where
+   a/b are the derivative orders on the row/column function; *table receives the id of the
+   deduplicated weight table.  Either output pointer may be NULL. */
+iga_status iga_lr_export_factor(const iga_lr_op* op, int32_t dir, int32_t factor_id, double* host_band,
+                                int32_t* pattern, int32_t* table);
+
+/* Human-readable message of the last failing call on this thread ("" if none). */
+const char* iga_last_error(void);
+
+/* Library version string. */
+const char* iga_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGA_LR_H */

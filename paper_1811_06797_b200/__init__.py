@@ -1,0 +1,262 @@
+"""B200-native low-rank IgA operator library (arXiv:1811.06797 hot path) — Python binding.
+
+Thin ctypes marshalling over the C ABI in ``include/iga_lr.h`` (``libigalr.so`` built in-tree
+by ``_build.py``).  Every step of the path runs in the library's CUDA kernels; PyTorch is used
+only for device memory (``tensor.data_ptr()``) and streams (``torch.cuda.Stream``).  There is
+no CPU fallback: if the shared library is missing this module raises ImportError, and every
+ABI failure raises ``IgaError`` with the library's message.
+
+Names follow the paper: ``mass`` = M (Eq. (massFinal)), ``stiff`` = K/S
+(Eq. (stiffnessFinal)), ``kkt_apply`` = Eq. (KKTSystem) PAPER.md:313-319.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libigalr.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        "libigalr.so not found in %s — build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(no CPU fallback exists)" % _HERE)
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+IGA_OK, IGA_EINVAL, IGA_ENOMEM, IGA_ECUDA, IGA_EUNSUPPORTED, IGA_ESTATE = range(6)
+IGA_DIRICHLET = 0x1
+PATHS = {"auto": 0x0, "unfused": 0x10, "fused": 0x20}
+STATUS_NAMES = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_ENOMEM", 3: "IGA_ECUDA", 4: "IGA_EUNSUPPORTED",
+                5: "IGA_ESTATE"}
+
+ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "iga_lr_apply", "iga_lr_apply2",
+               "iga_kkt_apply", "iga_lr_apply_host", "iga_kkt_apply_host", "iga_lr_info", "iga_lr_export_factor",
+               "iga_last_error", "iga_version"]
+
+
+class IgaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+
+
+class _Dir(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_int32), ("n", ctypes.c_int32), ("knots", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Space(ctypes.Structure):
+    _fields_ = [("dir", _Dir * 3), ("nq", ctypes.c_int32)]
+
+
+class _Sep(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_int32), ("coef", ctypes.POINTER(ctypes.c_double)),
+                ("tab", ctypes.POINTER(ctypes.c_double) * 3)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int64 * 3), ("p", ctypes.c_int32 * 3), ("nq", ctypes.c_int32),
+                ("n_factors", ctypes.c_int32 * 3), ("n_rounds", ctypes.c_int32), ("n_xprod", ctypes.c_int32),
+                ("n_yprod", ctypes.c_int32), ("n_zprod", ctypes.c_int32), ("has_mass", ctypes.c_int32),
+                ("has_stiff", ctypes.c_int32), ("fused_ok", ctypes.c_int32), ("plan_flops_per_vec", ctypes.c_double),
+                ("min_bytes_per_vec", ctypes.c_double)]
+
+
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_lib.iga_last_error.restype = ctypes.c_char_p
+_lib.iga_version.restype = ctypes.c_char_p
+_lib.iga_quad_nodes.argtypes = [ctypes.POINTER(_Space), ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int64)]
+_lib.iga_lr_assemble_factors.argtypes = [ctypes.POINTER(_Space), ctypes.POINTER(_Sep),
+                                         ctypes.POINTER(ctypes.POINTER(_Sep)), ctypes.c_uint32, _P,
+                                         ctypes.POINTER(_P)]
+_lib.iga_lr_destroy.argtypes = [_P]
+_lib.iga_lr_destroy.restype = None
+_lib.iga_lr_apply.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_uint32, _P]
+_lib.iga_lr_apply2.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_uint32,
+                               _P]
+_lib.iga_kkt_apply.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_uint32, _P]
+_lib.iga_lr_apply_host.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                   ctypes.c_uint32, _P]
+_lib.iga_kkt_apply_host.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_uint32,
+                                    _P]
+_lib.iga_lr_info.argtypes = [_P, ctypes.POINTER(_Info)]
+_lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.POINTER(ctypes.c_int32)]
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def version() -> str:
+    return _lib.iga_version().decode()
+
+
+def _check(rc: int):
+    if rc != IGA_OK:
+        raise IgaError(rc, _lib.iga_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _space(knots: Sequence[np.ndarray], p: Sequence[int], nq: int):
+    ks = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
+    sp = _Space()
+    for d in range(3):
+        sp.dir[d].p = int(p[d])
+        sp.dir[d].n = int(len(ks[d]) - int(p[d]) - 1)
+        sp.dir[d].knots = _dptr(ks[d])
+    sp.nq = int(nq)
+    return sp, ks
+
+
+def quad_nodes(knots: Sequence[np.ndarray], p: Sequence[int], nq: int = 0) -> List[np.ndarray]:
+    """Quadrature nodes of each direction (iga_quad_nodes): where weight tables are sampled."""
+    sp, keep = _space(knots, p, nq)
+    out = []
+    for d in range(3):
+        cnt = ctypes.c_int64(0)
+        _check(_lib.iga_quad_nodes(ctypes.byref(sp), d, None, ctypes.byref(cnt)))
+        buf = np.zeros(cnt.value)
+        _check(_lib.iga_quad_nodes(ctypes.byref(sp), d, _dptr(buf), ctypes.byref(cnt)))
+        out.append(buf)
+    return out
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _tensor_ptr(t, name: str) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("%s must be a torch.Tensor" % name)
+    if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError("%s must be a contiguous float64 CUDA tensor" % name)
+    return t.data_ptr()
+
+
+class SepWeight:
+    """Rank-R separable weight tabulated at the quadrature nodes (iga_sep):
+    f(x,y,z) = sum_r coef[r] tab[0][r](x) tab[1][r](y) tab[2][r](z)."""
+
+    def __init__(self, coef: Optional[np.ndarray], tabs: Sequence[np.ndarray]):
+        self.tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in tabs]
+        self.R = int(self.tabs[0].shape[0])
+        self.coef = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+
+    def _c(self) -> _Sep:
+        s = _Sep()
+        s.R = self.R
+        s.coef = _dptr(self.coef) if self.coef is not None else ctypes.POINTER(ctypes.c_double)()
+        for d in range(3):
+            s.tab[d] = _dptr(self.tabs[d])
+        return s
+
+
+class LowRankOperator:
+    """Mass and stiffness operators in low-rank Kronecker form on one GPU (iga_lr_op)."""
+
+    def __init__(self, knots: Sequence[np.ndarray], p: Sequence[int], omega: Optional[SepWeight],
+                 q: Optional[Sequence[Optional[SepWeight]]], nq: int = 0, dirichlet: bool = False, stream=None):
+        self._h = None
+        sp, keep = _space(knots, p, nq)
+        om = omega._c() if omega is not None else None
+        qarr = None
+        keep_q = []
+        if q is not None:
+            assert len(q) == 9
+            qarr = (ctypes.POINTER(_Sep) * 9)()
+            for b in range(9):
+                if q[b] is not None:
+                    s = q[b]._c()
+                    keep_q.append(s)
+                    qarr[b] = ctypes.pointer(s)
+        h = _P()
+        _check(_lib.iga_lr_assemble_factors(ctypes.byref(sp), ctypes.byref(om) if om is not None else None,
+                                            qarr, IGA_DIRICHLET if dirichlet else 0, _stream_handle(stream),
+                                            ctypes.byref(h)))
+        self._h = h
+        self.info = self._info()
+        self.dims = tuple(int(v) for v in self.info.dims)  # (mx, my, mz)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.iga_lr_destroy(self._h)
+            self._h = None
+
+    def _info(self) -> _Info:
+        inf = _Info()
+        _check(_lib.iga_lr_info(self._h, ctypes.byref(inf)))
+        return inf
+
+    @property
+    def ndof(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    def info_dict(self) -> dict:
+        i = self.info
+        return {"dims": list(i.dims), "p": list(i.p), "nq": i.nq, "n_factors": list(i.n_factors),
+                "n_rounds": i.n_rounds, "n_xprod": i.n_xprod, "n_yprod": i.n_yprod, "n_zprod": i.n_zprod,
+                "has_mass": bool(i.has_mass), "has_stiff": bool(i.has_stiff), "fused_ok": bool(i.fused_ok),
+                "plan_flops_per_vec": i.plan_flops_per_vec, "min_bytes_per_vec": i.min_bytes_per_vec}
+
+    def export_factor(self, d: int, fid: int) -> Tuple[np.ndarray, int, int]:
+        m = self.dims[d]
+        bw = 2 * self.info.p[d] + 1
+        band = np.zeros((m, bw))
+        pat = ctypes.c_int32(0)
+        tab = ctypes.c_int32(0)
+        _check(_lib.iga_lr_export_factor(self._h, d, fid, _dptr(band), ctypes.byref(pat), ctypes.byref(tab)))
+        return band, pat.value, tab.value
+
+    # ------------------------------------------------------------------ device applies
+    def apply(self, x, y_mass=None, y_stiff=None, alpha: float = 1.0, gamma: float = 1.0, path: str = "auto",
+              stream=None, batch: Optional[int] = None):
+        """y_mass = alpha M x, y_stiff = gamma S x on device tensors [batch, nz, ny, nx]."""
+        b = batch if batch is not None else (x.numel() // self.ndof)
+        _check(_lib.iga_lr_apply(self._h, _tensor_ptr(x, "x"),
+                                 _tensor_ptr(y_mass, "y_mass") if y_mass is not None else None,
+                                 _tensor_ptr(y_stiff, "y_stiff") if y_stiff is not None else None,
+                                 float(alpha), float(gamma), int(b), PATHS[path], _stream_handle(stream)))
+
+    def apply2(self, x_mass, x_stiff, out, alpha: float = 1.0, gamma: float = 1.0, path: str = "auto",
+               stream=None, batch: Optional[int] = None):
+        ref = x_mass if x_mass is not None else x_stiff
+        b = batch if batch is not None else (ref.numel() // self.ndof)
+        _check(_lib.iga_lr_apply2(self._h, _tensor_ptr(x_mass, "x_mass") if x_mass is not None else None,
+                                  _tensor_ptr(x_stiff, "x_stiff") if x_stiff is not None else None,
+                                  _tensor_ptr(out, "out"), float(alpha), float(gamma), int(b), PATHS[path],
+                                  _stream_handle(stream)))
+
+    def kkt_apply(self, X, out, n_t: int, tau: float, beta: float, path: str = "auto", stream=None):
+        """out = KKT(tau, beta, n_t) X for device tensors [3, n_t, nz, ny, nx] (Eq. (KKTSystem))."""
+        _check(_lib.iga_kkt_apply(self._h, int(n_t), float(tau), float(beta), _tensor_ptr(X, "X"),
+                                  _tensor_ptr(out, "out"), PATHS[path], _stream_handle(stream)))
+
+    # ------------------------------------------------------------------ host (end-to-end) applies
+    def apply_host(self, x: np.ndarray, y_mass: Optional[np.ndarray], y_stiff: Optional[np.ndarray],
+                   alpha: float = 1.0, gamma: float = 1.0, path: str = "auto", stream=None):
+        for a in (x, y_mass, y_stiff):
+            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous):
+                raise ValueError("host buffers must be C-contiguous float64")
+        b = x.size // self.ndof
+        _check(_lib.iga_lr_apply_host(self._h, x.ctypes.data, y_mass.ctypes.data if y_mass is not None else None,
+                                      y_stiff.ctypes.data if y_stiff is not None else None, float(alpha),
+                                      float(gamma), int(b), PATHS[path], _stream_handle(stream)))
+
+    def kkt_apply_host(self, X: np.ndarray, out: np.ndarray, n_t: int, tau: float, beta: float,
+                       path: str = "auto", stream=None):
+        _check(_lib.iga_kkt_apply_host(self._h, int(n_t), float(tau), float(beta), X.ctypes.data, out.ctypes.data,
+                                       PATHS[path], _stream_handle(stream)))

@@ -1,0 +1,592 @@
+// abi.cu — C ABI of libigalr (include/iga_lr.h): validation, Gauss rule, factor
+// deduplication, the shared-prefix evaluation plan, and dispatch of the CUDA kernels.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+namespace igalr {
+
+static thread_local std::string g_err;
+
+iga_status set_error(iga_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+iga_status cuda_error(cudaError_t e, const char* where) {
+    g_err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return IGA_ECUDA;
+}
+
+// ------------------------------------------------------------------------------------
+// Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence, reading G1/G2).
+static void gauss_legendre(int m, double* x, double* w) {
+    for (int k = 0; k < (m + 1) / 2; ++k) {
+        double t = std::cos(M_PI * (4.0 * k + 3.0) / (4.0 * m + 2.0));  // k-th largest root guess
+        double P = 0.0, dP = 1.0;
+        for (int it = 0; it < 64; ++it) {
+            double pm1 = 1.0, pc = t;  // P_0, P_1
+            for (int j = 2; j <= m; ++j) {
+                double pn = ((2 * j - 1) * t * pc - (j - 1) * pm1) / j;
+                pm1 = pc;
+                pc = pn;
+            }
+            if (m == 1) { pc = t; pm1 = 1.0; }
+            P = pc;
+            dP = m * (pm1 - t * pc) / (1.0 - t * t);
+            double dt = P / dP;
+            t -= dt;
+            if (std::fabs(dt) <= 1e-16 * std::fabs(t) + 1e-300) break;
+        }
+        double pm1 = 1.0, pc = t;
+        for (int j = 2; j <= m; ++j) {
+            double pn = ((2 * j - 1) * t * pc - (j - 1) * pm1) / j;
+            pm1 = pc;
+            pc = pn;
+        }
+        if (m == 1) { pc = t; pm1 = 1.0; }
+        dP = m * (pm1 - t * pc) / (1.0 - t * t);
+        const double wk = 2.0 / ((1.0 - t * t) * dP * dP);
+        x[m - 1 - k] = t;
+        w[m - 1 - k] = wk;
+        x[k] = -t;
+        w[k] = wk;
+    }
+    if (m % 2 == 1) x[m / 2] = 0.0;
+}
+
+static iga_status validate_dir(const iga_dir& d, int idx) {
+    char buf[256];
+    if (d.p < 1 || d.p > kMaxP) {
+        snprintf(buf, sizeof buf, "dir %d: degree p=%d outside supported 1..%d", idx, d.p, kMaxP);
+        return set_error(d.p < 1 ? IGA_EINVAL : IGA_EUNSUPPORTED, buf);
+    }
+    if (d.n < d.p + 1) {
+        snprintf(buf, sizeof buf, "dir %d: n=%d < p+1=%d", idx, d.n, d.p + 1);
+        return set_error(IGA_EINVAL, buf);
+    }
+    if (!d.knots) {
+        snprintf(buf, sizeof buf, "dir %d: knots is NULL", idx);
+        return set_error(IGA_EINVAL, buf);
+    }
+    const int L = d.n + d.p + 1;
+    for (int i = 0; i < L; ++i) {
+        double v = d.knots[i];
+        if (!std::isfinite(v) || v < 0.0 || v > 1.0) {
+            snprintf(buf, sizeof buf, "dir %d: knot %d = %g outside [0,1]", idx, i, v);
+            return set_error(IGA_EINVAL, buf);
+        }
+        if (i > 0 && v < d.knots[i - 1]) {
+            snprintf(buf, sizeof buf, "dir %d: knots decrease at %d", idx, i);
+            return set_error(IGA_EINVAL, buf);
+        }
+    }
+    for (int i = 0; i <= d.p; ++i)
+        if (d.knots[i] != 0.0 || d.knots[L - 1 - i] != 1.0) {
+            snprintf(buf, sizeof buf, "dir %d: knot vector is not open (first/last p+1 knots must be 0/1)", idx);
+            return set_error(IGA_EINVAL, buf);
+        }
+    // interior multiplicity <= p (Eq. (knotVector))
+    int run = 1;
+    for (int i = d.p + 1; i < d.n; ++i) {
+        run = (d.knots[i] == d.knots[i - 1] && i - 1 > d.p) ? run + 1 : 1;
+        if (d.knots[i] > 0.0 && d.knots[i] < 1.0 && run > d.p) {
+            snprintf(buf, sizeof buf, "dir %d: interior knot %g has multiplicity > p", idx, d.knots[i]);
+            return set_error(IGA_EINVAL, buf);
+        }
+    }
+    return IGA_OK;
+}
+
+static iga_status validate_space(const iga_space* sp) {
+    if (!sp) return set_error(IGA_EINVAL, "space is NULL");
+    for (int d = 0; d < 3; ++d) {
+        iga_status s = validate_dir(sp->dir[d], d);
+        if (s) return s;
+    }
+    if (sp->nq < 0 || sp->nq > kMaxNq) return set_error(IGA_EUNSUPPORTED, "nq outside 0..16");
+    return IGA_OK;
+}
+
+static int nq_of(const iga_space* sp, int d) { return sp->nq ? sp->nq : sp->dir[d].p + 1; }
+
+static DirQuad build_quad(const iga_dir& d, int nq) {
+    DirQuad q;
+    q.n = d.n;
+    q.p = d.p;
+    q.nq = nq;
+    q.knots.assign(d.knots, d.knots + d.n + d.p + 1);
+    double gx[kMaxNq], gw[kMaxNq];
+    gauss_legendre(nq, gx, gw);
+    for (int s = d.p; s < d.n; ++s) {
+        const double a = q.knots[s], b = q.knots[s + 1];
+        if (!(a < b)) continue;
+        q.span.push_back(s);
+        const double h = b - a;
+        for (int k = 0; k < nq; ++k) {
+            q.node.push_back(a + 0.5 * h * (gx[k] + 1.0));
+            q.wgt.push_back(0.5 * h * gw[k]);
+        }
+    }
+    q.ne = (int)q.span.size();
+    return q;
+}
+
+// nnz of the kept banded 1D matrix (all band positions inside the matrix)
+static double nnz1(int m, int p) {
+    double s = 0;
+    for (int i = 0; i < m; ++i) s += std::min(i + p, m - 1) - std::max(i - p, 0) + 1;
+    return s;
+}
+
+struct Term {
+    int part;      // 0 mass, 1 stiffness
+    int f[3];      // factor ids x, y, z
+    double c;
+};
+
+// Greedy packing of terms (in r-major order) into rounds of bounded shape.
+static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, bool split_slots, Plan* pl) {
+    // merge identical terms (same part, factors, and slot semantics)
+    std::vector<Term> terms;
+    for (const Term& t : terms_in) {
+        bool merged = false;
+        for (Term& u : terms)
+            if (u.part == t.part && u.f[0] == t.f[0] && u.f[1] == t.f[1] && u.f[2] == t.f[2]) {
+                u.c += t.c;
+                merged = true;
+                break;
+            }
+        if (!merged) terms.push_back(t);
+    }
+    pl->rounds.clear();
+    Round cur;
+    memset(&cur, 0, sizeof cur);
+    auto flush = [&]() {
+        if (cur.ng) pl->rounds.push_back(cur);
+        memset(&cur, 0, sizeof cur);
+    };
+    for (const Term& t : terms) {
+        if (t.c == 0.0) continue;
+        const int slot = split_slots ? t.part : 0;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            int xe = -1, pe = -1, ge = -1;
+            for (int i = 0; i < cur.nx; ++i)
+                if (cur.xf[i] == t.f[0] && cur.xslot[i] == slot) xe = i;
+            int need_x = xe < 0;
+            if (!need_x)
+                for (int j = 0; j < cur.np; ++j)
+                    if (cur.pf[j] == t.f[1] && cur.px[j] == xe) pe = j;
+            int need_p = pe < 0;
+            for (int g = 0; g < cur.ng; ++g)
+                if (cur.gf[g] == t.f[2] && cur.gpart[g] == t.part) ge = g;
+            int need_g = ge < 0;
+            int need_e = 1;
+            if (ge >= 0 && pe >= 0)
+                for (int e = 0; e < cur.ne[ge]; ++e)
+                    if (cur.ep[ge][e] == pe) need_e = 0;
+            bool fits = cur.nx + need_x <= kMaxX && cur.np + need_p <= kMaxPair && cur.ng + need_g <= kMaxG &&
+                        (need_g || cur.ne[ge] + need_e <= kMaxE);
+            if (!fits) {
+                flush();
+                continue;
+            }
+            if (need_x) {
+                xe = cur.nx++;
+                cur.xf[xe] = t.f[0];
+                cur.xslot[xe] = slot;
+            }
+            if (need_p) {
+                pe = cur.np++;
+                cur.pf[pe] = t.f[1];
+                cur.px[pe] = xe;
+            }
+            if (need_g) {
+                ge = cur.ng++;
+                cur.gf[ge] = t.f[2];
+                cur.gpart[ge] = t.part;
+                cur.ne[ge] = 0;
+            }
+            int ee = -1;
+            for (int e = 0; e < cur.ne[ge]; ++e)
+                if (cur.ep[ge][e] == pe) ee = e;
+            if (ee < 0) {
+                ee = cur.ne[ge]++;
+                cur.ep[ge][ee] = pe;
+                cur.ec[ge][ee] = 0.0;
+            }
+            cur.ec[ge][ee] += t.c;
+            break;
+        }
+    }
+    flush();
+    pl->n_x = pl->n_y = pl->n_z = 0;
+    for (const Round& r : pl->rounds) {
+        pl->n_x += r.nx;
+        pl->n_y += r.np;
+        pl->n_z += r.ng;
+    }
+    const double N = (double)op->m[0] * op->m[1] * op->m[2];
+    pl->flops = 2.0 * (pl->n_x * nnz1(op->m[0], op->p[0]) * (N / op->m[0]) +
+                       pl->n_y * nnz1(op->m[1], op->p[1]) * (N / op->m[1]) +
+                       pl->n_z * nnz1(op->m[2], op->p[2]) * (N / op->m[2]));
+    pl->fused_ok = fused_supported(op, *pl);
+}
+
+static iga_status check_sep(const iga_sep* s, const int* nn, const char* what) {
+    char buf[200];
+    if (s->R < 1) {
+        snprintf(buf, sizeof buf, "%s: R=%d < 1", what, s->R);
+        return set_error(IGA_EINVAL, buf);
+    }
+    for (int d = 0; d < 3; ++d) {
+        if (!s->tab[d]) {
+            snprintf(buf, sizeof buf, "%s: tab[%d] is NULL", what, d);
+            return set_error(IGA_EINVAL, buf);
+        }
+        for (long long i = 0; i < (long long)s->R * nn[d]; ++i)
+            if (!std::isfinite(s->tab[d][i])) {
+                snprintf(buf, sizeof buf, "%s: non-finite table value (dir %d)", what, d);
+                return set_error(IGA_EINVAL, buf);
+            }
+    }
+    if (s->coef)
+        for (int r = 0; r < s->R; ++r)
+            if (!std::isfinite(s->coef[r])) {
+                snprintf(buf, sizeof buf, "%s: non-finite coef", what);
+                return set_error(IGA_EINVAL, buf);
+            }
+    return IGA_OK;
+}
+
+}  // namespace igalr
+
+using namespace igalr;
+
+extern "C" {
+
+const char* iga_last_error(void) { return g_err.c_str(); }
+
+const char* iga_version(void) { return "igalr 0.1 (sm_100a)"; }
+
+iga_status iga_quad_nodes(const iga_space* sp, int32_t dir, double* nodes_out, int64_t* nnodes) {
+    g_err.clear();
+    if (iga_status s = validate_space(sp)) return s;
+    if (dir < 0 || dir > 2) return set_error(IGA_EINVAL, "dir must be 0..2");
+    if (!nnodes) return set_error(IGA_EINVAL, "nnodes is NULL");
+    DirQuad q = build_quad(sp->dir[dir], nq_of(sp, dir));
+    *nnodes = (int64_t)q.node.size();
+    if (nodes_out) memcpy(nodes_out, q.node.data(), sizeof(double) * q.node.size());
+    return IGA_OK;
+}
+
+iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, const iga_sep* const* q, uint32_t flags,
+                                   void* stream, iga_lr_op** out) {
+    g_err.clear();
+    if (!out) return set_error(IGA_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (iga_status s = validate_space(sp)) return s;
+    if (flags & ~IGA_DIRICHLET) return set_error(IGA_EINVAL, "unknown flags");
+    const bool dir = (flags & IGA_DIRICHLET) != 0;
+    for (int d = 0; d < 3; ++d)
+        if (dir && sp->dir[d].n < 3) return set_error(IGA_EINVAL, "Dirichlet elimination needs n >= 3");
+    bool any_q = false;
+    if (q)
+        for (int b = 0; b < 9; ++b) any_q |= q[b] != nullptr;
+    if (!omega && !any_q) return set_error(IGA_EINVAL, "neither mass nor stiffness weight given");
+    cudaStream_t st = (cudaStream_t)stream;
+
+    DirQuad quad[3];
+    int nn[3];
+    for (int d = 0; d < 3; ++d) {
+        quad[d] = build_quad(sp->dir[d], nq_of(sp, d));
+        nn[d] = (int)quad[d].node.size();
+    }
+    if (omega)
+        if (iga_status s = check_sep(omega, nn, "omega")) return s;
+    if (q)
+        for (int b = 0; b < 9; ++b)
+            if (q[b]) {
+                char w[16];
+                snprintf(w, sizeof w, "q[%d]", b);
+                if (iga_status s = check_sep(q[b], nn, w)) return s;
+            }
+
+    // Deduplicate weight tables and (table, pattern) factors per direction.
+    std::vector<std::vector<double>> tables[3];
+    std::vector<FactorSpec> specs[3];
+    auto table_id = [&](int d, const double* t) {
+        for (size_t i = 0; i < tables[d].size(); ++i)
+            if (memcmp(tables[d][i].data(), t, sizeof(double) * nn[d]) == 0) return (int)i;
+        tables[d].emplace_back(t, t + nn[d]);
+        return (int)tables[d].size() - 1;
+    };
+    auto factor_id = [&](int d, int tab, int a, int b) {
+        for (size_t i = 0; i < specs[d].size(); ++i)
+            if (specs[d][i].table == tab && specs[d][i].a == a && specs[d][i].b == b) return (int)i;
+        specs[d].push_back({tab, a, b});
+        return (int)specs[d].size() - 1;
+    };
+    // Terms in r-major order: mass r, then stiffness blocks (k,l) for the same r.
+    std::vector<Term> terms;
+    int maxR = omega ? omega->R : 0;
+    if (q)
+        for (int b = 0; b < 9; ++b)
+            if (q[b]) maxR = std::max(maxR, (int)q[b]->R);
+    for (int r = 0; r < maxR; ++r) {
+        if (omega && r < omega->R) {
+            Term t;
+            t.part = 0;
+            t.c = omega->coef ? omega->coef[r] : 1.0;
+            for (int d = 0; d < 3; ++d) t.f[d] = factor_id(d, table_id(d, omega->tab[d] + (size_t)r * nn[d]), 0, 0);
+            terms.push_back(t);
+        }
+        if (q)
+            for (int b = 0; b < 9; ++b) {
+                if (!q[b] || r >= q[b]->R) continue;
+                const int k = b / 3, l = b % 3;  // K_ij = sum_kl q_kl d_l beta_i d_k beta_j
+                Term t;
+                t.part = 1;
+                t.c = q[b]->coef ? q[b]->coef[r] : 1.0;
+                for (int d = 0; d < 3; ++d)
+                    t.f[d] = factor_id(d, table_id(d, q[b]->tab[d] + (size_t)r * nn[d]), l == d ? 1 : 0, k == d ? 1 : 0);
+                terms.push_back(t);
+            }
+    }
+
+    iga_lr_op* op = new (std::nothrow) iga_lr_op();
+    if (!op) return set_error(IGA_ENOMEM, "host allocation failed");
+    cudaGetDevice(&op->device);
+    op->nq = sp->nq ? sp->nq : 0;
+    op->dirichlet = dir;
+    op->has_mass = omega != nullptr;
+    op->has_stiff = any_q;
+    for (int d = 0; d < 3; ++d) {
+        op->n[d] = sp->dir[d].n;
+        op->p[d] = sp->dir[d].p;
+        op->m[d] = dir ? op->n[d] - 2 : op->n[d];
+    }
+    for (int d = 0; d < 3; ++d) {
+        iga_status s = assemble_dir(quad[d], tables[d], specs[d], dir, st, &op->F[d]);
+        if (s) {
+            iga_lr_destroy(op);
+            return s;
+        }
+    }
+    std::vector<Term> tm, ts;
+    for (auto& t : terms) (t.part == 0 ? tm : ts).push_back(t);
+    build_plan(op, terms, false, &op->plan[kPlanBoth]);
+    build_plan(op, terms, true, &op->plan[kPlanBothSplit]);
+    build_plan(op, tm, false, &op->plan[kPlanMass]);
+    build_plan(op, ts, false, &op->plan[kPlanStiff]);
+    const double N = (double)op->m[0] * op->m[1] * op->m[2];
+    op->min_bytes = 8.0 * N * (1 + (op->has_mass ? 1 : 0) + (op->has_stiff ? 1 : 0));
+    *out = op;
+    return IGA_OK;
+}
+
+void iga_lr_destroy(iga_lr_op* op) {
+    if (!op) return;
+    for (int d = 0; d < 3; ++d)
+        if (op->F[d].band) cudaFree(op->F[d].band);
+    delete op;
+}
+
+static iga_status check_ptr(const void* p, const char* what) {
+    if (((uintptr_t)p) & 7) return set_error(IGA_EINVAL, std::string(what) + " is not 8-byte aligned");
+    return IGA_OK;
+}
+
+static iga_status run_plan(const iga_lr_op* op, PlanKind kind, const OutMap& om, int batch, uint32_t flags,
+                           cudaStream_t st) {
+    const Plan& pl = op->plan[kind];
+    const uint32_t path = flags & (IGA_PATH_UNFUSED | IGA_PATH_FUSED);
+    if (path == IGA_PATH_FUSED && !pl.fused_ok)
+        return set_error(IGA_EUNSUPPORTED, "fused kernel does not support this plan/degree");
+    if (path != IGA_PATH_UNFUSED && pl.fused_ok) return apply_fused(op, pl, om, batch, st);
+    return apply_unfused(op, pl, om, batch, st);
+}
+
+iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out, double alpha,
+                         double gamma, int32_t batch, uint32_t flags, void* stream) {
+    g_err.clear();
+    if (!op) return set_error(IGA_EINVAL, "op is NULL");
+    if (!out) return set_error(IGA_EINVAL, "out is NULL");
+    if (batch < 1) return set_error(IGA_EINVAL, "batch < 1");
+    if (!x_mass && !x_stiff) return set_error(IGA_EINVAL, "both inputs NULL");
+    if (x_mass && !op->has_mass) return set_error(IGA_ESTATE, "op has no mass part");
+    if (x_stiff && !op->has_stiff) return set_error(IGA_ESTATE, "op has no stiffness part");
+    if (out == x_mass || out == x_stiff) return set_error(IGA_EINVAL, "output aliases an input");
+    for (const void* p : {(const void*)x_mass, (const void*)x_stiff, (const void*)out})
+        if (iga_status s = check_ptr(p, "pointer")) return s;
+    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED)) return set_error(IGA_EINVAL, "unknown flags");
+    OutMap om;
+    om.src[0] = x_mass;
+    om.src[1] = x_stiff;
+    om.dst[0] = x_mass ? out : nullptr;
+    om.dst[1] = x_stiff ? out : nullptr;
+    om.scale[0] = alpha;
+    om.scale[1] = gamma;
+    PlanKind kind = (x_mass && x_stiff) ? (x_mass == x_stiff ? kPlanBoth : kPlanBothSplit) : (x_mass ? kPlanMass : kPlanStiff);
+    if (kind == kPlanMass || kind == kPlanStiff) {
+        om.dst[0] = om.dst[1] = out;
+        om.src[0] = om.src[1] = x_mass ? x_mass : x_stiff;
+    }
+    if (kind == kPlanBoth) om.dst[0] = om.dst[1] = out;
+    return run_plan(op, kind, om, batch, flags, (cudaStream_t)stream);
+}
+
+iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, double* y_stiff, double alpha,
+                        double gamma, int32_t batch, uint32_t flags, void* stream) {
+    g_err.clear();
+    if (!op) return set_error(IGA_EINVAL, "op is NULL");
+    if (!x) return set_error(IGA_EINVAL, "x is NULL");
+    if (batch < 1) return set_error(IGA_EINVAL, "batch < 1");
+    if (!y_mass && !y_stiff) return set_error(IGA_EINVAL, "no output requested");
+    if (y_mass && !op->has_mass) return set_error(IGA_ESTATE, "op has no mass part");
+    if (y_stiff && !op->has_stiff) return set_error(IGA_ESTATE, "op has no stiffness part");
+    if ((const double*)y_mass == x || (const double*)y_stiff == x) return set_error(IGA_EINVAL, "output aliases x");
+    for (const void* p : {(const void*)x, (const void*)y_mass, (const void*)y_stiff})
+        if (iga_status s = check_ptr(p, "pointer")) return s;
+    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED)) return set_error(IGA_EINVAL, "unknown flags");
+    OutMap om;
+    om.src[0] = om.src[1] = x;
+    om.dst[0] = y_mass;
+    om.dst[1] = y_stiff;
+    om.scale[0] = alpha;
+    om.scale[1] = gamma;
+    PlanKind kind = (y_mass && y_stiff) ? kPlanBoth : (y_mass ? kPlanMass : kPlanStiff);
+    if (kind != kPlanBoth) om.dst[0] = om.dst[1] = (y_mass ? y_mass : y_stiff);
+    return run_plan(op, kind, om, batch, flags, (cudaStream_t)stream);
+}
+
+iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in, double* out,
+                         uint32_t flags, void* stream) {
+    g_err.clear();
+    if (!op) return set_error(IGA_EINVAL, "op is NULL");
+    if (!op->has_mass || !op->has_stiff) return set_error(IGA_ESTATE, "KKT needs mass and stiffness");
+    if (n_t < 1) return set_error(IGA_EINVAL, "n_t < 1");
+    if (!(tau > 0.0) || !std::isfinite(tau)) return set_error(IGA_EINVAL, "tau must be > 0");
+    if (!(beta > 0.0) || !std::isfinite(beta)) return set_error(IGA_EINVAL, "beta must be > 0");
+    if (!in || !out) return set_error(IGA_EINVAL, "NULL in/out");
+    if (in == out) return set_error(IGA_EINVAL, "in and out alias");
+    if (check_ptr(in, "in") || check_ptr(out, "out")) return IGA_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = (int64_t)op->m[0] * op->m[1] * op->m[2];
+    const size_t blk = (size_t)n_t * N;
+    double* abc = nullptr;  // a, b, c combos [3][n_t][N]
+    cudaError_t e = cudaMallocAsync(&abc, sizeof(double) * 3 * blk, st);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
+    iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);
+    // r_y = M b + tau S lambda ; r_u = tau M a ; r_lambda = M c + tau S y
+    if (!s) s = iga_lr_apply2(op, abc + blk, in + 2 * blk, out, 1.0, tau, n_t, flags, stream);
+    if (!s) s = iga_lr_apply2(op, abc, nullptr, out + blk, tau, 0.0, n_t, flags, stream);
+    if (!s) s = iga_lr_apply2(op, abc + 2 * blk, in, out + 2 * blk, 1.0, tau, n_t, flags, stream);
+    cudaFreeAsync(abc, st);
+    return s;
+}
+
+static iga_status host_roundtrip(size_t in_elems, size_t out_elems, int nout, const double* in_h, double** out_h,
+                                 cudaStream_t st, double** d_in, double** d_out) {
+    cudaError_t e = cudaMallocAsync(d_in, sizeof(double) * in_elems, st);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(host in)");
+    e = cudaMallocAsync(d_out, sizeof(double) * out_elems * nout, st);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(host out)");
+    e = cudaMemcpyAsync(*d_in, in_h, sizeof(double) * in_elems, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_error(e, "H2D");
+    (void)out_h;
+    return IGA_OK;
+}
+
+iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host, double* y_stiff_host,
+                             double alpha, double gamma, int32_t batch, uint32_t flags, void* stream) {
+    g_err.clear();
+    if (!op || !x_host || batch < 1 || (!y_mass_host && !y_stiff_host)) return set_error(IGA_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t tot = (size_t)op->m[0] * op->m[1] * op->m[2] * batch;
+    double *d_in = nullptr, *d_out = nullptr;
+    const bool same = y_mass_host && y_mass_host == y_stiff_host;
+    int nout = same ? 1 : (y_mass_host ? 1 : 0) + (y_stiff_host ? 1 : 0);
+    iga_status s = host_roundtrip(tot, tot, nout, x_host, nullptr, st, &d_in, &d_out);
+    double* dm = y_mass_host ? d_out : nullptr;
+    double* ds = y_stiff_host ? (same ? d_out : d_out + (y_mass_host ? tot : 0)) : nullptr;
+    if (!s) s = iga_lr_apply(op, d_in, dm, ds, alpha, gamma, batch, flags, stream);
+    cudaError_t e = cudaSuccess;
+    if (!s && y_mass_host) e = cudaMemcpyAsync(y_mass_host, dm, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
+    if (!s && !e && y_stiff_host && !same) e = cudaMemcpyAsync(y_stiff_host, ds, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
+    if (d_in) cudaFreeAsync(d_in, st);
+    if (d_out) cudaFreeAsync(d_out, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (s) return s;
+    if (e) return cuda_error(e, "D2H");
+    if (e2) return cuda_error(e2, "stream sync");
+    return IGA_OK;
+}
+
+iga_status iga_kkt_apply_host(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in_host,
+                              double* out_host, uint32_t flags, void* stream) {
+    g_err.clear();
+    if (!op || !in_host || !out_host || n_t < 1) return set_error(IGA_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t tot = (size_t)op->m[0] * op->m[1] * op->m[2] * n_t * 3;
+    double *d_in = nullptr, *d_out = nullptr;
+    iga_status s = host_roundtrip(tot, tot, 1, in_host, nullptr, st, &d_in, &d_out);
+    if (!s) s = iga_kkt_apply(op, n_t, tau, beta, d_in, d_out, flags, stream);
+    cudaError_t e = cudaSuccess;
+    if (!s) e = cudaMemcpyAsync(out_host, d_out, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
+    if (d_in) cudaFreeAsync(d_in, st);
+    if (d_out) cudaFreeAsync(d_out, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (s) return s;
+    if (e) return cuda_error(e, "D2H");
+    if (e2) return cuda_error(e2, "stream sync");
+    return IGA_OK;
+}
+
+iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info) {
+    g_err.clear();
+    if (!op || !info) return set_error(IGA_EINVAL, "NULL argument");
+    memset(info, 0, sizeof *info);
+    const Plan& pl = op->plan[op->has_mass && op->has_stiff ? kPlanBoth : (op->has_mass ? kPlanMass : kPlanStiff)];
+    for (int d = 0; d < 3; ++d) {
+        info->dims[d] = op->m[d];
+        info->p[d] = op->p[d];
+        info->n_factors[d] = op->F[d].nf;
+    }
+    info->nq = op->nq ? op->nq : op->p[0] + 1;
+    info->n_rounds = (int32_t)pl.rounds.size();
+    info->n_xprod = pl.n_x;
+    info->n_yprod = pl.n_y;
+    info->n_zprod = pl.n_z;
+    info->has_mass = op->has_mass;
+    info->has_stiff = op->has_stiff;
+    info->fused_ok = pl.fused_ok;
+    info->plan_flops_per_vec = pl.flops;
+    info->min_bytes_per_vec = op->min_bytes;
+    return IGA_OK;
+}
+
+iga_status iga_lr_export_factor(const iga_lr_op* op, int32_t dir, int32_t factor_id, double* host_band,
+                                int32_t* pattern, int32_t* table) {
+    g_err.clear();
+    if (!op || dir < 0 || dir > 2) return set_error(IGA_EINVAL, "bad op/dir");
+    const DirFactors& F = op->F[dir];
+    if (factor_id < 0 || factor_id >= F.nf) return set_error(IGA_EINVAL, "factor_id out of range");
+    if (pattern) *pattern = F.pattern[factor_id];
+    if (table) *table = F.table[factor_id];
+    if (host_band) {
+        cudaError_t e = cudaMemcpy(host_band, F.band + (size_t)factor_id * F.m * F.bw, sizeof(double) * F.m * F.bw,
+                                   cudaMemcpyDeviceToHost);
+        if (e) return cuda_error(e, "export D2H");
+    }
+    return IGA_OK;
+}
+
+}  // extern "C"

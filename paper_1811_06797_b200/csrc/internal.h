@@ -1,0 +1,109 @@
+// internal.h — shared declarations of libigalr (host planning + CUDA kernels).
+// Not part of the ABI (see include/iga_lr.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "iga_lr.h"
+
+namespace igalr {
+
+constexpr int kMaxP = 6;        // compiled degree range 1..kMaxP
+constexpr int kMaxNq = 16;      // Gauss points per span
+constexpr int kMaxBW = 2 * kMaxP + 1;
+
+// Plan round limits (shared-prefix evaluation).
+constexpr int kMaxX = 5;   // x-entries (factor, input slot) per round
+constexpr int kMaxPair = 10;  // (y factor, x-entry) pairs per round
+constexpr int kMaxG = 5;   // z groups (z factor, output part) per round
+constexpr int kMaxE = 4;   // (pair, coef) entries per group
+
+// One round of the evaluation plan.  Everything a kernel needs is POD, passed by value.
+struct Round {
+    int nx;
+    int xf[kMaxX];      // factor id in direction x
+    int xslot[kMaxX];   // input slot: 0 = mass input, 1 = stiffness input
+    int np;
+    int pf[kMaxPair];   // factor id in direction y
+    int px[kMaxPair];   // x-entry index
+    int ng;
+    int gf[kMaxG];      // factor id in direction z
+    int gpart[kMaxG];   // 0 = mass part, 1 = stiffness part
+    int ne[kMaxG];
+    int ep[kMaxG][kMaxE];     // pair index
+    double ec[kMaxG][kMaxE];  // coefficient
+};
+
+struct DirFactors {
+    int m = 0;        // kept extent (n or n-2)
+    int p = 0;
+    int bw = 0;       // 2p+1
+    int nf = 0;       // number of distinct factors
+    double* band = nullptr;  // device [nf][m][bw], band[f][i][k] = F[i][i-p+k]
+    std::vector<int> pattern;  // a*2+b per factor
+    std::vector<int> table;    // dedup weight-table id per factor
+};
+
+// Per-call output routing for kernels: groups of part g go to dst[g] with scale[g].
+struct OutMap {
+    double* dst[2];   // output pointers for part 0 (mass) and 1 (stiffness); may alias
+    double scale[2];
+    const double* src[2];  // input pointer for slot 0 (mass) and slot 1 (stiffness)
+};
+
+}  // namespace igalr
+
+namespace igalr {
+// An evaluation plan: rounds + its algorithmic cost.  The op keeps one per request kind.
+struct Plan {
+    std::vector<Round> rounds;
+    int n_x = 0, n_y = 0, n_z = 0;  // mode products per vector
+    double flops = 0;               // algorithmic flops per vector (2 * nnz per mode product)
+    bool fused_ok = false;
+};
+enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kNumPlans = 4 };
+}  // namespace igalr
+
+struct iga_lr_op {
+    int n[3], p[3], m[3], nq;
+    bool dirichlet;
+    bool has_mass, has_stiff;
+    igalr::DirFactors F[3];
+    igalr::Plan plan[igalr::kNumPlans];
+    double min_bytes = 0;
+    int device = 0;
+};
+
+namespace igalr {
+
+// ---- error plumbing (abi.cu)
+iga_status set_error(iga_status s, const std::string& msg);
+iga_status cuda_error(cudaError_t e, const char* where);
+
+// ---- factor assembly (factors.cu)
+struct DirQuad {
+    int n, p, nq, ne;
+    std::vector<double> knots;
+    std::vector<int> span;       // [ne] knot-span index s of each nonempty span (first fn = s-p)
+    std::vector<double> node;    // [ne*nq]
+    std::vector<double> wgt;     // [ne*nq] Gauss weight * span length / 2
+};
+struct FactorSpec {
+    int table;    // weight table id (rows of `tables`)
+    int a, b;     // derivative order on row / column function
+};
+iga_status assemble_dir(const DirQuad& q, const std::vector<std::vector<double>>& tables,
+                        const std::vector<FactorSpec>& specs, bool dirichlet, cudaStream_t st,
+                        DirFactors* out);
+
+// ---- apply kernels
+iga_status apply_unfused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
+iga_status apply_fused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
+bool fused_supported(const iga_lr_op* op, const Plan& pl);
+iga_status kkt_combos(const double* in, double* abc, int n_t, int64_t N, double tau, double beta,
+                      cudaStream_t st);
+
+}  // namespace igalr
