@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py — GDoF/s of the fp64 low-rank Kronecker operator apply on B200 (+ % of roofline).
+
+Default workload: BASELINE config c3 (128^3, p=3, R=8, mass + full anisotropic stiffness,
+batch of 8 N(0,1) vectors) — the first full-size config the >= 70 % roofline target is
+quoted on.  A "step" = one mass+stiffness apply (steps A6-A8 of SURVEY §8(a)) of the whole
+batch; factor assembly (A1-A5) runs once before timing and is reported as setup_ms.  The other
+configs (c2, c4 KKT, c5) are timed the same way and reported under "configs".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank applies its own batch (weak scaling, the
+batch dimension shards with no collective); time = max over ranks.
+--impl reference times the CPU oracle (row-restricted bilinear form) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAK_FP64_TFLOPS = 37.0  # measured: tools/ubench.cu DMMA/DFMA (profiles/r01_ubench.md); nominal 37.2 @1965 MHz
+
+
+def _measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, v: float) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------- GPU arm
+def time_workload(cfgname: str, steps: int, warmup: int, ws: int, path: str = "auto", e2e: bool = True):
+    import torch
+    from paper_1811_06797_b200 import workloads
+    cfg = synth.CONFIGS[cfgname]
+    knots, w, x = synth.draw_problem(cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = workloads.build_operator(cfg, w)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t0) * 1e3
+    info = op.info_dict()
+    stream = torch.cuda.Stream()
+    xd = torch.from_numpy(x).cuda()
+    N = op.ndof
+    with torch.cuda.stream(stream):
+        if cfg.kkt:
+            out = torch.empty_like(xd)
+            run = lambda: op.kkt_apply(xd, out, cfg.n_t, cfg.tau, cfg.beta, path=path, stream=stream)
+            dof = 3 * cfg.n_t * N
+            flops = cfg.n_t * (op_kkt_flops(op))
+        else:
+            ym = torch.empty_like(xd)
+            ys = torch.empty_like(xd)
+            run = lambda: op.apply(xd, ym, ys, path=path, stream=stream)
+            dof = cfg.batch * N
+            flops = cfg.batch * info["plan_flops_per_vec"]
+    for _ in range(warmup):
+        run()
+    stream.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with ClockSampler(torch.cuda.current_device()) as cs:
+        for i in range(steps):
+            ev[i][0].record(stream)
+            run()
+            ev[i][1].record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    barrier(ws)
+    per = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(per)
+    tot_ms = allmax(ws, tot_ms)
+    ms = tot_ms / steps
+    res = {"cfg": cfg, "op": op, "info": info, "ms": ms, "min_ms": min(per), "dof": dof, "flops": flops,
+           "setup_ms": setup_ms, "clocks": cs.summary(), "x": x, "stream": stream}
+    if e2e and not cfg.kkt:
+        # end to end through the public host API: pinned host buffers, H2D + apply + D2H per step
+        xh = torch.from_numpy(x).pin_memory()
+        ymh = torch.empty_like(xh).pin_memory()
+        ysh = torch.empty_like(xh).pin_memory()
+        xn, ymn, ysn = xh.numpy(), ymh.numpy(), ysh.numpy()
+        op.apply_host(xn, ymn, ysn, path=path, stream=stream)
+        barrier(ws)
+        t0 = time.perf_counter()
+        k = max(1, min(steps, 5))
+        for _ in range(k):
+            op.apply_host(xn, ymn, ysn, path=path, stream=stream)
+        e2e_s = allmax(ws, (time.perf_counter() - t0) / k)
+        res["e2e"] = {"value": ws * dof / e2e_s / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": int(x.nbytes),
+                      "d2h_bytes_per_step": int(2 * x.nbytes)}
+    elif e2e and cfg.kkt:
+        xh = torch.from_numpy(x).pin_memory()
+        oh = torch.empty_like(xh).pin_memory()
+        op.kkt_apply_host(xh.numpy(), oh.numpy(), cfg.n_t, cfg.tau, cfg.beta, path=path, stream=stream)
+        t0 = time.perf_counter()
+        k = max(1, min(steps, 5))
+        for _ in range(k):
+            op.kkt_apply_host(xh.numpy(), oh.numpy(), cfg.n_t, cfg.tau, cfg.beta, path=path, stream=stream)
+        e2e_s = allmax(ws, (time.perf_counter() - t0) / k)
+        res["e2e"] = {"value": ws * dof / e2e_s / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": int(x.nbytes),
+                      "d2h_bytes_per_step": int(x.nbytes)}
+    return res
+
+
+def op_kkt_flops(op) -> float:
+    """Algorithmic flops of one KKT time step: 3 mass applies + 2 stiffness applies (43R plan)."""
+    i = op.info_dict()
+    return i["plan_flops_mass"] * 3 + i["plan_flops_stiff"] * 2 if "plan_flops_mass" in i else 0.0
+
+
+def launches_per_step(info: dict, path: str, kkt: bool) -> int:
+    if info["fused_ok"] and path != "unfused":
+        return 4 if kkt else 1
+    r = info["n_rounds"]
+    return (1 + 3 * 3 * r) if kkt else 3 * r
+
+
+# ----------------------------------------------------------------------------------- CPU arm
+def cpu_oracle_rate(cfgname: str, seconds: float = 12.0):
+    """Oracle (row-restricted bilinear form, OpenMP on all host cores) on a bounded sample of
+    rows of the workload: GDoF/s = output rows (mass+stiffness) per second."""
+    import oracle
+    cfg = synth.CONFIGS[cfgname]
+    knots, w, x = synth.draw_problem(cfg)
+    P = oracle.problem_from_config(cfg, w)
+    rng = np.random.default_rng(0)
+    N = P.ndof
+    done = 0
+    t0 = time.perf_counter()
+    chunk = 256
+    xv = x.reshape(-1, N) if not cfg.kkt else x.reshape(-1, N)
+    while time.perf_counter() - t0 < seconds:
+        rows = rng.integers(0, N, chunk)
+        oracle.apply_rows(P, xv[done // chunk % xv.shape[0]], rows)
+        done += chunk
+    el = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    kind_rows = done * (1 if not cfg.kkt else 1)
+    return {"value": kind_rows / el / 1e9, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
+            "sample": "%d random output rows (mass+stiffness) of %s, %.1f s" % (done, cfgname, el)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="auto", choices=["auto", "fused", "unfused"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    a = ap.parse_args()
+    warmup = max(3, a.warmup)
+
+    if a.impl == "reference":
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        per = []
+        for _ in range(max(1, min(a.steps, 3))):
+            per.append(cpu_oracle_rate(a.config, seconds=max(2.0, a.cpu_seconds / 3)))
+        val = statistics.median(p["value"] for p in per)
+        cfg = synth.CONFIGS[a.config]
+        line = {"metric": "GDoF/s of fp64 low-rank Kronecker operator/KKT apply; % of roofline",
+                "impl": "reference", "value": val, "unit": "GDoF/s", "n_gpus": a.gpus, "steps": len(per),
+                "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": cfg.name, "global_batch": cfg.batch},
+                "cpu_baseline": dict(per[0], value=val),
+                "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    ws, rank, local = dist_setup()
+    import torch
+    torch.cuda.set_device(local)
+    from paper_1811_06797_b200 import workloads  # noqa: F401  (fails loudly without the .so)
+    res = time_workload(a.config, a.steps, warmup, ws, path=a.path)
+    cfg = res["cfg"]
+    ms = res["ms"]
+    value = ws * res["dof"] / (ms * 1e-3) / 1e9
+    achieved = res["flops"] / (ms * 1e-3) / 1e12
+    peak = PEAK_FP64_TFLOPS
+    launches = launches_per_step(res["info"], a.path, cfg.kkt)
+    line = {
+        "metric": "GDoF/s of fp64 low-rank Kronecker operator/KKT apply; % of roofline",
+        "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": a.steps, "warmup": warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded N(0,1) inputs, seeded separable sine weights; DESIGN.md §3)",
+        "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "R": cfg.R, "batch_per_gpu": cfg.batch,
+                   "global_batch": cfg.batch * ws, "parallelism": "dp%d (batch sharded, no collective)" % ws,
+                   "path": a.path, "l2": "inputs (%.0f MB) larger than L2 (126 MB); no flush" % (res["x"].nbytes / 1e6)},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": "FP64 DFMA pipe; peak measured by tools/ubench (DFMA/DMMA 37.0 TF/s); achieved = "
+                             "plan algorithmic flops / CUDA-event step time"},
+        "gpu_launches": launches * a.steps,
+        "clocks": res["clocks"],
+        "setup_ms": res["setup_ms"],
+        "plan": {k: res["info"][k] for k in ("n_rounds", "n_xprod", "n_yprod", "n_zprod", "plan_flops_per_vec",
+                                              "fused_ok")},
+    }
+    if "e2e" in res:
+        line["e2e"] = res["e2e"]
+    if rank == 0 and ws == 1 and not a.no_extra:
+        extra = {}
+        for other in ("c2", "c5", "c4"):
+            if other == a.config:
+                continue
+            try:
+                r2 = time_workload(other, max(3, a.steps // 2), 3, 1, path=a.path, e2e=False)
+                v2 = r2["dof"] / (r2["ms"] * 1e-3) / 1e9
+                ach = r2["flops"] / (r2["ms"] * 1e-3) / 1e12 if r2["flops"] else None
+                extra[other] = {"workload": r2["cfg"].name, "GDoF_s": v2, "ms": r2["ms"],
+                                "tflops": ach, "frac": (ach / peak) if ach else None}
+                del r2
+                torch.cuda.empty_cache()
+            except Exception as e:  # report, never hide
+                extra[other] = {"error": repr(e)}
+        line["configs"] = extra
+    if rank == 0 and ws == 1:
+        line["cpu_baseline"] = cpu_oracle_rate(a.config, seconds=a.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -82,6 +82,7 @@ typedef struct {
 #define IGA_PATH_AUTO 0x0u      /* fused sm_100a kernel when the plan fits, else unfused */
 #define IGA_PATH_UNFUSED 0x10u  /* one launch per mode-product stage through HBM scratch */
 #define IGA_PATH_FUSED 0x20u    /* fused kernel; IGA_EUNSUPPORTED if the plan does not fit */
+#define IGA_PATH_FUSED_V1 0x40u /* force the first-generation fused kernel (testing) */
 
 /* Quadrature nodes of direction dir (0..2): nq-point Gauss-Legendre on each nonempty span,
    ascending.  nodes_out may be NULL to query *nnodes (= nonempty spans * nq). HOST memory. */
@@ -141,9 +142,12 @@ typedef struct {
     int32_t n_rounds;            /* plan rounds (shared-prefix evaluation groups) */
     int32_t n_xprod, n_yprod, n_zprod; /* mode products per vector in the plan */
     int32_t has_mass, has_stiff;
-    int32_t fused_ok;            /* 1 if the fused kernel supports this plan */
+    int32_t fused_ok;            /* 1 if the first-generation fused kernel supports this plan */
+    int32_t fused2_ok;           /* 1 if the TMEM-ring fused kernel (v2) supports every part */
     double plan_flops_per_vec;   /* algorithmic flops of one mass+stiffness apply of one vector */
     double min_bytes_per_vec;    /* 8 * (1 input + outputs) * N */
+    double plan_flops_mass;      /* ... of a mass-only apply of one vector */
+    double plan_flops_stiff;     /* ... of a stiffness-only apply of one vector */
 } iga_lr_info_t;
 
 iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info);

@@ -29,7 +29,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 IGA_OK, IGA_EINVAL, IGA_ENOMEM, IGA_ECUDA, IGA_EUNSUPPORTED, IGA_ESTATE = range(6)
 IGA_DIRICHLET = 0x1
-PATHS = {"auto": 0x0, "unfused": 0x10, "fused": 0x20}
+PATHS = {"auto": 0x0, "unfused": 0x10, "fused": 0x20, "fused_v1": 0x40}
 STATUS_NAMES = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_ENOMEM", 3: "IGA_ECUDA", 4: "IGA_EUNSUPPORTED",
                 5: "IGA_ESTATE"}
 
@@ -61,8 +61,9 @@ class _Info(ctypes.Structure):
     _fields_ = [("dims", ctypes.c_int64 * 3), ("p", ctypes.c_int32 * 3), ("nq", ctypes.c_int32),
                 ("n_factors", ctypes.c_int32 * 3), ("n_rounds", ctypes.c_int32), ("n_xprod", ctypes.c_int32),
                 ("n_yprod", ctypes.c_int32), ("n_zprod", ctypes.c_int32), ("has_mass", ctypes.c_int32),
-                ("has_stiff", ctypes.c_int32), ("fused_ok", ctypes.c_int32), ("plan_flops_per_vec", ctypes.c_double),
-                ("min_bytes_per_vec", ctypes.c_double)]
+                ("has_stiff", ctypes.c_int32), ("fused_ok", ctypes.c_int32), ("fused2_ok", ctypes.c_int32), ("plan_flops_per_vec", ctypes.c_double),
+                ("min_bytes_per_vec", ctypes.c_double), ("plan_flops_mass", ctypes.c_double),
+                ("plan_flops_stiff", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -209,8 +210,9 @@ class LowRankOperator:
         i = self.info
         return {"dims": list(i.dims), "p": list(i.p), "nq": i.nq, "n_factors": list(i.n_factors),
                 "n_rounds": i.n_rounds, "n_xprod": i.n_xprod, "n_yprod": i.n_yprod, "n_zprod": i.n_zprod,
-                "has_mass": bool(i.has_mass), "has_stiff": bool(i.has_stiff), "fused_ok": bool(i.fused_ok),
-                "plan_flops_per_vec": i.plan_flops_per_vec, "min_bytes_per_vec": i.min_bytes_per_vec}
+                "has_mass": bool(i.has_mass), "has_stiff": bool(i.has_stiff), "fused_ok": bool(i.fused_ok), "fused2_ok": bool(i.fused2_ok),
+                "plan_flops_per_vec": i.plan_flops_per_vec, "min_bytes_per_vec": i.min_bytes_per_vec,
+                "plan_flops_mass": i.plan_flops_mass, "plan_flops_stiff": i.plan_flops_stiff}
 
     def export_factor(self, d: int, fid: int) -> Tuple[np.ndarray, int, int]:
         m = self.dims[d]

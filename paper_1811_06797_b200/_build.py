@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
-SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "kkt.cu"]
+SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_fused2.cu", "kkt.cu"]
 
 
 def _newer(src_paths, target):

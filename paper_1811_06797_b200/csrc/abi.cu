@@ -153,7 +153,12 @@ struct Term {
 };
 
 // Greedy packing of terms (in r-major order) into rounds of bounded shape.
-static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, bool split_slots, Plan* pl) {
+struct Limits {
+    int x = kMaxX, p = kMaxPair, g = kMaxG, e = kMaxE, t = 1 << 20;  // t: total (pair,group) entries
+};
+
+static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, bool split_slots, Plan* pl,
+                       Limits lim = Limits(), bool fused_v1 = true) {
     // merge identical terms (same part, factors, and slot semantics)
     std::vector<Term> terms;
     for (const Term& t : terms_in) {
@@ -192,8 +197,10 @@ static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, b
             if (ge >= 0 && pe >= 0)
                 for (int e = 0; e < cur.ne[ge]; ++e)
                     if (cur.ep[ge][e] == pe) need_e = 0;
-            bool fits = cur.nx + need_x <= kMaxX && cur.np + need_p <= kMaxPair && cur.ng + need_g <= kMaxG &&
-                        (need_g || cur.ne[ge] + need_e <= kMaxE);
+            int tot_e = 0;
+            for (int g = 0; g < cur.ng; ++g) tot_e += cur.ne[g];
+            bool fits = cur.nx + need_x <= lim.x && cur.np + need_p <= lim.p && cur.ng + need_g <= lim.g &&
+                        (need_g || cur.ne[ge] + need_e <= lim.e) && tot_e + need_e <= lim.t;
             if (!fits) {
                 flush();
                 continue;
@@ -237,7 +244,8 @@ static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, b
     pl->flops = 2.0 * (pl->n_x * nnz1(op->m[0], op->p[0]) * (N / op->m[0]) +
                        pl->n_y * nnz1(op->m[1], op->p[1]) * (N / op->m[1]) +
                        pl->n_z * nnz1(op->m[2], op->p[2]) * (N / op->m[2]));
-    pl->fused_ok = fused_supported(op, *pl);
+    pl->fused_ok = fused_v1 && fused_supported(op, *pl);
+    if (pl->fused_ok && prepare_fused(op, pl) != IGA_OK) pl->fused_ok = false;
 }
 
 static iga_status check_sep(const iga_sep* s, const int* nn, const char* what) {
@@ -386,6 +394,25 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     build_plan(op, terms, true, &op->plan[kPlanBothSplit]);
     build_plan(op, tm, false, &op->plan[kPlanMass]);
     build_plan(op, ts, false, &op->plan[kPlanStiff]);
+    if (fused2_supported(op)) {
+        Limits lm;
+        lm.x = lm.p = lm.g = lm.e = lm.t = 1;
+        Limits ls;
+        ls.x = 4;
+        ls.p = 9;
+        ls.g = 4;
+        ls.e = 9;
+        ls.t = 9;
+        if (op->has_mass) {
+            build_plan(op, tm, false, &op->plan[kPlanF2Mass], lm, false);
+            if (prepare_fused2(op, &op->plan[kPlanF2Mass], 0) != IGA_OK) op->plan[kPlanF2Mass].f2_ok = false;
+        }
+        if (op->has_stiff) {
+            build_plan(op, ts, false, &op->plan[kPlanF2Stiff], ls, false);
+            if (prepare_fused2(op, &op->plan[kPlanF2Stiff], 1) != IGA_OK) op->plan[kPlanF2Stiff].f2_ok = false;
+        }
+        g_err.clear();
+    }
     const double N = (double)op->m[0] * op->m[1] * op->m[2];
     op->min_bytes = 8.0 * N * (1 + (op->has_mass ? 1 : 0) + (op->has_stiff ? 1 : 0));
     *out = op;
@@ -396,6 +423,10 @@ void iga_lr_destroy(iga_lr_op* op) {
     if (!op) return;
     for (int d = 0; d < 3; ++d)
         if (op->F[d].band) cudaFree(op->F[d].band);
+    for (int k = 0; k < kNumPlans; ++k) {
+        release_fused(&op->plan[k]);
+        if (op->plan[k].d_f2) cudaFree(op->plan[k].d_f2);
+    }
     delete op;
 }
 
@@ -407,11 +438,31 @@ static iga_status check_ptr(const void* p, const char* what) {
 static iga_status run_plan(const iga_lr_op* op, PlanKind kind, const OutMap& om, int batch, uint32_t flags,
                            cudaStream_t st) {
     const Plan& pl = op->plan[kind];
-    const uint32_t path = flags & (IGA_PATH_UNFUSED | IGA_PATH_FUSED);
-    if (path == IGA_PATH_FUSED && !pl.fused_ok)
+    const uint32_t path = flags & (IGA_PATH_UNFUSED | IGA_PATH_FUSED | 0x40u);
+    if ((path == IGA_PATH_FUSED || path == 0x40u) && !pl.fused_ok)
         return set_error(IGA_EUNSUPPORTED, "fused kernel does not support this plan/degree");
     if (path != IGA_PATH_UNFUSED && pl.fused_ok) return apply_fused(op, pl, om, batch, st);
     return apply_unfused(op, pl, om, batch, st);
+}
+
+// Fused-v2 routing: one launch per part (mass, stiffness); returns IGA_EUNSUPPORTED (no
+// side effects) when a needed part has no fused-v2 plan.
+static iga_status run_f2(const iga_lr_op* op, const double* xm, const double* xs, double* dm, double* ds, double alpha,
+                         double gamma, int batch, cudaStream_t st) {
+    const bool need_m = xm && dm, need_s = xs && ds;
+    if (need_m && !op->plan[kPlanF2Mass].f2_ok) return IGA_EUNSUPPORTED;
+    if (need_s && !op->plan[kPlanF2Stiff].f2_ok) return IGA_EUNSUPPORTED;
+    iga_status s = IGA_OK;
+    if (need_m) s = apply_fused2_part(op, op->plan[kPlanF2Mass], 0, xm, dm, alpha, 0, batch, st);
+    if (!s && need_s)
+        s = apply_fused2_part(op, op->plan[kPlanF2Stiff], 1, xs, ds, gamma, (need_m && dm == ds) ? 1 : 0, batch, st);
+    return s;
+}
+
+static bool want_f2(const iga_lr_op* op, int batch, uint32_t flags) {
+    const uint32_t path = flags & (IGA_PATH_UNFUSED | IGA_PATH_FUSED | 0x40u);
+    if (path == IGA_PATH_FUSED) return true;
+    return path == IGA_PATH_AUTO && fused2_preferred(op, batch);
 }
 
 iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out, double alpha,
@@ -426,7 +477,13 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
     if (out == x_mass || out == x_stiff) return set_error(IGA_EINVAL, "output aliases an input");
     for (const void* p : {(const void*)x_mass, (const void*)x_stiff, (const void*)out})
         if (iga_status s = check_ptr(p, "pointer")) return s;
-    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED)) return set_error(IGA_EINVAL, "unknown flags");
+    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED | 0x40u)) return set_error(IGA_EINVAL, "unknown flags");
+    if (want_f2(op, batch, flags)) {
+        iga_status s = run_f2(op, x_mass, x_stiff, x_mass ? out : nullptr, x_stiff ? out : nullptr, alpha, gamma, batch,
+                              (cudaStream_t)stream);
+        if (s != IGA_EUNSUPPORTED) return s;
+        g_err.clear();
+    }
     OutMap om;
     om.src[0] = x_mass;
     om.src[1] = x_stiff;
@@ -455,7 +512,13 @@ iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, do
     if ((const double*)y_mass == x || (const double*)y_stiff == x) return set_error(IGA_EINVAL, "output aliases x");
     for (const void* p : {(const void*)x, (const void*)y_mass, (const void*)y_stiff})
         if (iga_status s = check_ptr(p, "pointer")) return s;
-    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED)) return set_error(IGA_EINVAL, "unknown flags");
+    if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED | 0x40u)) return set_error(IGA_EINVAL, "unknown flags");
+    if (want_f2(op, batch, flags)) {
+        iga_status s = run_f2(op, y_mass ? x : nullptr, y_stiff ? x : nullptr, y_mass, y_stiff, alpha, gamma, batch,
+                              (cudaStream_t)stream);
+        if (s != IGA_EUNSUPPORTED) return s;
+        g_err.clear();
+    }
     OutMap om;
     om.src[0] = om.src[1] = x;
     om.dst[0] = y_mass;
@@ -568,8 +631,11 @@ iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info) {
     info->has_mass = op->has_mass;
     info->has_stiff = op->has_stiff;
     info->fused_ok = pl.fused_ok;
+    info->fused2_ok = (!op->has_mass || op->plan[kPlanF2Mass].f2_ok) && (!op->has_stiff || op->plan[kPlanF2Stiff].f2_ok);
     info->plan_flops_per_vec = pl.flops;
     info->min_bytes_per_vec = op->min_bytes;
+    info->plan_flops_mass = op->has_mass ? op->plan[kPlanMass].flops : 0.0;
+    info->plan_flops_stiff = op->has_stiff ? op->plan[kPlanStiff].flops : 0.0;
     return IGA_OK;
 }
 

@@ -1,0 +1,679 @@
+// apply_fused2.cu — fused sm_100a apply, version 2: TMEM-resident z-ring.
+//
+// One part (mass OR stiffness) per launch:
+//   y(z,y,x) = sum_rounds sum_g Fz_g *_z  sum_{j in g} c_j  Fy_j *_y  Fx_{e(j)} *_x  v
+// (Eqs. (massFinal)/(stiffnessFinal)).
+//
+// CTA = 4 warps (one per TMEM lane quadrant), tile = 128 x-columns x L y-rows of one batch
+// vector.  Persistent CTAs walk a contiguous range of (tile, z-plane) units; for every input
+// plane z' and plan round r each thread (one x-column) sweeps the L+2P rows of its column:
+//   X: t_e(y') = sum_k Fx_e[x][k] v(y', x-P+k)  (x-coefs in registers, v from the smem tile)
+//   Y: sliding register window over t_e; u_j = sum_k Fy_j[y][k] t_{e(j)}(y-P+k) (y-coefs are
+//      smem broadcasts), G_g = sum_j c_j u_j
+//   Z: ring(y,x)[slot] += Cz[g][slot] G_g  — the ring of 2P+1 output planes per point lives in
+//      TMEM (tcgen05.ld/st, 32x32b); slots are physical (plane mod 2P+1), the z-coefficients
+//      are permuted per z' instead of rotating the ring.
+// A plane is retired inline during the last round once its last input plane is processed.
+// Planes whose inputs span two CTAs' ranges are written to per-CTA scratch and summed by
+// k_fixup in CTA order (deterministic; no atomics).
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace igalr {
+namespace f2 {
+
+constexpr int TXW = 32;          // columns per warp
+constexpr int NW = 4;            // warps per CTA (one per TMEM lane quadrant)
+constexpr int TX = TXW * NW;     // 128 columns per tile
+constexpr int kMaxRounds2 = 40;
+
+template <int NX, int NP, int NG>
+struct Round2 {
+    int nx, np, ng, nyf;
+    int xf[NX];        // x factor of x-entry e
+    int yf[NP];        // distinct y factors of the round (nyf of them)
+    int pyf[NP];       // pair -> y-factor slot
+    int px[NP];        // pair -> x-entry
+    int pg[NP];        // pair -> group
+    int plead[NP];     // 1 if the pair is its group's lead (coef folded into the group scale)
+    double pc[NP];     // pair coefficient / group scale (unused for lead pairs)
+    int gf[NG];        // group z factor
+    double gs[NG];     // group scale (lead pair coefficient)
+};
+
+struct Args2 {
+    const double* src;
+    double* dst;
+    double scale;
+    int accumulate;
+    double* scratch;       // [nctas][NSEG][4P][L][TX] partial planes
+    const double* bx;
+    const double* by;
+    const double* bz;
+    const void* rounds;
+    int nrounds;
+    int mx, my, mz, batch;
+    int tiles_x, tiles_y;
+    long long units;       // tiles * mz
+    int nctas;
+};
+
+constexpr int NSEG = 4;    // max segments per CTA (checked on the host)
+
+__host__ __device__ inline long long unit_begin(long long k, long long units, int nctas) {
+    return k * units / nctas;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- TMEM helpers (32x32b shape: each thread accesses its own lane)
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, double* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const double* v) {
+    uint32_t r[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        r[2 * k] = __double2loint(v[k]);
+        r[2 * k + 1] = __double2hiint(v[k]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, double* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    v[0] = __hiloint2double(r[1], r[0]);
+    v[1] = __hiloint2double(r[3], r[2]);
+}
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const double* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__double2loint(v[0])),
+                 "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ring slots per point, padded to a multiple of 8 doubles (x16 loads) or +2 (x4 tail)
+template <int BW>
+struct RingShape {
+    static constexpr int REM = BW % 8;
+    static constexpr int N16 = BW / 8 + (REM >= 5 ? 1 : 0);     // number of x16 chunks (8 doubles)
+    static constexpr int N4 = (REM >= 5 || REM == 0) ? 0 : (REM + 1) / 2;  // x4 chunks (2 doubles)
+    static constexpr int DBL = N16 * 8 + N4 * 2;  // doubles stored per point
+    static constexpr int COLS = DBL * 2;          // TMEM columns per point
+};
+
+template <int BW>
+__device__ __forceinline__ void ring_ld(uint32_t t, double* v) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) tm_ld16(t + c * 16, v + c * 8);
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) tm_ld4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+}
+template <int BW>
+__device__ __forceinline__ void ring_st(uint32_t t, const double* v) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) tm_st16(t + c * 16, v + c * 8);
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) tm_st4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+}
+
+template <int P, int L>
+struct Geo {
+    static constexpr int BW = 2 * P + 1;
+    static constexpr int HY = L + 2 * P;          // sweep rows (incl. y-halo)
+    static constexpr int HX = TX + 2 * P;         // tile columns incl. x-halo
+    static constexpr int HXP = HX + 1;            // padded row pitch
+};
+
+// scratch slot of a partial output plane zo for a segment [za, zb) (see header comment)
+__device__ __forceinline__ int partial_slot(int zo, int za, int zb, int P) {
+    const int rel = zo - (za - P);
+    if (rel < 2 * P) return rel;                  // head band
+    return 2 * P + (zo - (zb - P));               // tail band
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+__global__ void __launch_bounds__(NW * 32, 1) k_fused2(const Args2 a) {
+    using G_ = Geo<P, L>;
+    constexpr int BW = G_::BW, HY = G_::HY, HXP = G_::HXP;
+    using RS = RingShape<BW>;
+    using RoundT = Round2<NX, NP, NG>;
+    static_assert(L * RS::COLS <= 512, "ring does not fit in TMEM");
+
+    extern __shared__ __align__(16) double sm[];
+    double* vin = sm;                                   // [2][HY][HXP]
+    double* xcs = vin + 2 * HY * HXP;                   // [2][NX][TX][BW]
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nrounds][NY][L][BW]  (by y-factor slot)
+    double* zcs = ycs + (size_t)a.nrounds * NY * L * BW;  // [2][nrounds][NG][BW]
+    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cx = warp * TXW + lane;  // tile column of this thread
+
+    // ---- TMEM allocation (512 columns, one CTA per SM)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < a.nrounds * (int)(sizeof(RoundT) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(rs)[i] = reinterpret_cast<const int*>(a.rounds)[i];
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(warp * 32) << 16);
+
+    const long long plane = (long long)a.mx * a.my;
+    const long long u0 = unit_begin(blockIdx.x, a.units, a.nctas);
+    const long long u1 = unit_begin(blockIdx.x + 1, a.units, a.nctas);
+
+    int seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / a.mz;
+        const int za = (int)(u - tile * a.mz);
+        const int zb = (int)min((long long)a.mz, (long long)za + (u1 - u));
+        u += zb - za;
+        long long tt = tile;
+        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+        const int b = (int)tt;
+        const int x0 = txi * TX, y0 = tyi * L;
+        const long long vb = (long long)b * a.mz * plane;
+        const int gx = x0 + cx;
+
+        // ---- stage y-coefficients of this tile (all rounds), clear the ring
+        __syncthreads();
+        for (int r = 0; r < a.nrounds; ++r) {
+            const RoundT& R = rs[r];
+            for (int i = threadIdx.x; i < R.nyf * L * BW; i += blockDim.x) {
+                const int s = i / (L * BW), rem = i - s * L * BW;
+                const int row = rem / BW, k = rem - row * BW;
+                const int gy = y0 + row;
+                const bool ok = gy < a.my;
+                cp8(ycs + ((size_t)(r * NY + s) * L + row) * BW + k,
+                    ok ? a.by + ((size_t)R.yf[s] * a.my + gy) * BW + k : a.by, ok);
+            }
+        }
+        {
+            double zero[RS::DBL];
+#pragma unroll
+            for (int k = 0; k < RS::DBL; ++k) zero[k] = 0.0;
+            for (int i = 0; i < L; ++i) ring_st<BW>(tbase + i * RS::COLS, zero);
+        }
+
+        auto stage_plane = [&](int zp, int buf) {
+            double* dstp = vin + buf * HY * HXP;
+            const double* srcp = a.src + vb + (long long)zp * plane;
+            for (int i = threadIdx.x; i < HY * G_::HX; i += blockDim.x) {
+                const int r = i / G_::HX, c = i - r * G_::HX;
+                const int gy = y0 - P + r, gxx = x0 - P + c;
+                const bool ok = gy >= 0 && gy < a.my && gxx >= 0 && gxx < a.mx;
+                cp8(dstp + r * HXP + c, ok ? srcp + (long long)gy * a.mx + gxx : a.src, ok);
+            }
+            // z-coefficients of plane zp for all rounds, permuted to physical ring slots:
+            // slot j holds output plane zo with zo == j (mod BW); coefficient Fz[zo][zp - zo + P]
+            double* zdst = zcs + buf * a.nrounds * NG * BW;
+            for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
+                const int r = i / (NG * BW), rem = i - r * NG * BW;
+                const int g = rem / BW, j = rem - g * BW;
+                const RoundT& R = rs[r];
+                int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;  // plane in [zp-P, zp+P] with zo%BW == j
+                const bool ok = g < R.ng && zo >= 0 && zo < a.mz;
+                cp8(zdst + i, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
+            }
+        };
+        auto stage_xc = [&](int r, int buf) {
+            const RoundT& R = rs[r];
+            double* dstp = xcs + buf * NX * TX * BW;
+            for (int i = threadIdx.x; i < R.nx * TX * BW; i += blockDim.x) {
+                const int e = i / (TX * BW), rem = i - e * TX * BW;
+                const int c = rem / BW, k = rem - c * BW;
+                const int g = x0 + c;
+                const bool ok = g < a.mx;
+                cp8(dstp + i, ok ? a.bx + ((size_t)R.xf[e] * a.mx + g) * BW + k : a.bx, ok);
+            }
+        };
+
+        const int zlo = za, zhi = zb;
+        stage_plane(zlo, 0);
+        stage_xc(0, 0);
+        cp_commit();
+        int pbuf = 0, xbuf = 0;
+        for (int zp = zlo; zp < zhi; ++zp) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                // prefetch: next round's x-coefs (and the next plane at the start of the plane)
+                const bool last_round = (r == a.nrounds - 1);
+                cp_wait<0>();
+                tm_wait_st();
+                __syncthreads();
+                if (!last_round) {
+                    stage_xc(r + 1, xbuf ^ 1);
+                } else if (zp + 1 < zhi) {
+                    stage_xc(0, xbuf ^ 1);
+                }
+                if (r == 0 && zp + 1 < zhi) stage_plane(zp + 1, pbuf ^ 1);
+                cp_commit();
+
+                const RoundT& R = rs[r];
+                const double* vt = vin + pbuf * HY * HXP;
+                const double* xc = xcs + xbuf * NX * TX * BW;
+                const double* yc = ycs + (size_t)r * NY * L * BW;
+                const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
+                double xr[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) xr[e][k] = (e < R.nx) ? xc[(e * TX + cx) * BW + k] : 0.0;
+                double zr[NG][BW];
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                    for (int j = 0; j < BW; ++j) zr[g][j] = (g < R.ng) ? zc[g * BW + j] * R.gs[g] : 0.0;
+                // retire slot of output plane zp - P in the last round (if complete here)
+                const int zret = zp - P;
+                const int jret = ((zret % BW) + BW) % BW;
+                bool ret_valid = false, ret_complete = false;
+                if (last_round && zret >= 0 && zret < a.mz) {
+                    ret_valid = true;
+                    const int lo = max(0, zret - P), hi = min(a.mz - 1, zret + P);
+                    ret_complete = lo >= za && hi <= zb - 1;
+                }
+
+                double w[NX][BW];  // circular window of t_e over the last BW rows
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) w[e][k] = 0.0;
+
+#pragma unroll 1
+                for (int base = 0; base < HY; base += BW) {
+#pragma unroll
+                    for (int q = 0; q < BW; ++q) {
+                        const int step = base + q;
+                        if (step < HY) {
+                            // X stage for sweep row `step`
+                            double v[BW];
+#pragma unroll
+                            for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + cx + k];
+#pragma unroll
+                            for (int e = 0; e < NX; ++e) {
+                                double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                                for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
+#pragma unroll
+                                for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
+                                w[e][q] = acc0 + acc1;
+                            }
+                            if (step >= 2 * P) {
+                                const int i = step - 2 * P;  // output row in tile
+                                const uint32_t tp = tbase + i * RS::COLS;
+                                double ring[RS::DBL];
+                                ring_ld<BW>(tp, ring);
+                                double G[NG];
+#pragma unroll
+                                for (int g = 0; g < NG; ++g) G[g] = 0.0;
+                                const double* ycr = yc + (size_t)i * BW;
+#pragma unroll
+                                for (int j = 0; j < NP; ++j) {
+                                    if (j < R.np) {
+                                        const double* fy = ycr + (size_t)R.pyf[j] * L * BW;
+                                        const int e = R.px[j];
+                                        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+                                        for (int ee = 0; ee < NX; ++ee) {
+                                            if (ee == e) {
+#pragma unroll
+                                                for (int k = 0; k < BW; k += 2) u0 = fma(fy[k], w[ee][(q + 1 + k) % BW], u0);
+#pragma unroll
+                                                for (int k = 1; k < BW; k += 2) u1 = fma(fy[k], w[ee][(q + 1 + k) % BW], u1);
+                                            }
+                                        }
+                                        const double u = u0 + u1;
+                                        const int g = R.pg[j];
+#pragma unroll
+                                        for (int gg = 0; gg < NG; ++gg)
+                                            if (gg == g) G[gg] = R.plead[j] ? G[gg] + u : fma(R.pc[j], u, G[gg]);
+                                    }
+                                }
+#pragma unroll
+                                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                                if (ret_valid) {
+                                    double val = 0.0;
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j)
+                                        if (j == jret) {
+                                            val = ring[j];
+                                            ring[j] = 0.0;
+                                        }
+                                    const int gy = y0 + i;
+                                    if (gy < a.my && gx < a.mx) {
+                                        if (ret_complete) {
+                                            const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                            a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                        } else {
+                                            const int slot = partial_slot(zret, za, zb, P);
+                                            a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx] =
+                                                a.scale * val;
+                                        }
+                                    }
+                                }
+                                ring_st<BW>(tp, ring);
+                            }
+                        }
+                    }
+                }
+                if (last_round) pbuf ^= 1;
+                xbuf ^= 1;
+            }
+        }
+        // ---- flush planes still in the ring: zo in [zb-P, zb+P) (partial unless zb == mz)
+        tm_wait_st();
+        __syncthreads();
+        for (int i = 0; i < L; ++i) {
+            const uint32_t tp = tbase + i * RS::COLS;
+            double ring[RS::DBL];
+            ring_ld<BW>(tp, ring);
+            const int gy = y0 + i;
+#pragma unroll
+            for (int s = 0; s < 2 * P; ++s) {
+                const int zo = zb - P + s;
+                if (zo < 0 || zo >= a.mz || zo < za - P) continue;
+                // already retired inline? planes zo <= zb-1-P were retired during the sweep
+                if (zo <= zb - 1 - P) continue;
+                const int j = zo % BW;
+                double val = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BW; ++jj)
+                    if (jj == j) val = ring[jj];
+                if (gy < a.my && gx < a.mx) {
+                    const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+                    const bool complete = lo >= za && hi <= zb - 1;
+                    if (complete) {
+                        const long long o = vb + (long long)zo * plane + (long long)gy * a.mx + gx;
+                        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                    } else {
+                        const int slot = partial_slot(zo, za, zb, P);
+                        a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx] = a.scale * val;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
+}
+
+// Sum partial planes: for every (tile, zo) whose inputs span several CTA ranges, add the
+// contributions of those CTAs in increasing CTA order.
+__global__ void k_fixup(const Args2 a, int P, int L) {
+    const long long plane = (long long)a.mx * a.my;
+    const int ntile = a.tiles_x * a.tiles_y * a.batch;
+    const long long total = (long long)ntile * a.mz * L * TX;
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
+        const int cx = (int)(g % TX);
+        const int i = (int)((g / TX) % L);
+        const int zo = (int)((g / ((long long)TX * L)) % a.mz);
+        const long long tile = g / ((long long)TX * L * a.mz);
+        long long tt = tile;
+        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+        const int b = (int)tt;
+        const int gx = txi * TX + cx, gy = tyi * L + i;
+        if (gx >= a.mx || gy >= a.my) continue;
+        const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+        const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
+        // CTA owning unit ulo / uhi
+        long long k0 = (ulo * a.nctas) / a.units;
+        while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
+        while (unit_begin(k0 + 1, a.units, a.nctas) <= ulo) ++k0;
+        long long k1 = (uhi * a.nctas) / a.units;
+        while (k1 > 0 && unit_begin(k1, a.units, a.nctas) > uhi) --k1;
+        while (unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
+        if (k0 == k1) continue;  // complete inside one CTA segment: written by k_fused2
+        double s = 0.0;
+        for (long long k = k0; k <= k1; ++k) {
+            // segment index of `tile` inside CTA k, and its [za, zb)
+            const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
+            int seg = 0;
+            int za = 0, zb = 0;
+            bool found = false;
+            for (long long u = cu0; u < cu1; ++seg) {
+                const long long t2 = u / a.mz;
+                const int sa = (int)(u - t2 * a.mz);
+                const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
+                if (t2 == tile) {
+                    za = sa;
+                    zb = sb;
+                    found = true;
+                    break;
+                }
+                u += sb - sa;
+            }
+            if (!found) continue;
+            const int slot = partial_slot(zo, za, zb, P);
+            s += a.scratch[((((size_t)k * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx];
+        }
+        const long long o = (long long)b * a.mz * plane + (long long)zo * plane + (long long)gy * a.mx + gx;
+        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + s;
+    }
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+size_t smem_bytes(int nrounds) {
+    using G_ = Geo<P, L>;
+    constexpr int BW = G_::BW;
+    return sizeof(double) * (2 * G_::HY * G_::HXP + 2 * NX * TX * BW + (size_t)nrounds * NY * L * BW +
+                             2 * (size_t)nrounds * NG * BW) +
+           sizeof(Round2<NX, NP, NG>) * nrounds + 64;
+}
+
+}  // namespace f2
+
+// ---------------------------------------------------------------------------------- host
+namespace {
+
+template <int NX, int NP, int NG, int NY>
+bool build_rounds2(const Plan& pl, std::vector<f2::Round2<NX, NP, NG>>* out) {
+    out->clear();
+    for (const Round& R : pl.rounds) {
+        // split pairs that feed several groups into one pair per group
+        f2::Round2<NX, NP, NG> F;
+        memset(&F, 0, sizeof F);
+        if (R.nx > NX || R.ng > NG) return false;
+        F.nx = R.nx;
+        F.ng = R.ng;
+        for (int e = 0; e < R.nx; ++e) F.xf[e] = R.xf[e];
+        for (int g = 0; g < R.ng; ++g) F.gf[g] = R.gf[g];
+        int np = 0;
+        bool lead_done[kMaxG] = {false, false, false, false, false};
+        for (int g = 0; g < R.ng; ++g) {
+            for (int e = 0; e < R.ne[g]; ++e) {
+                if (np >= NP) return false;
+                const int j = R.ep[g][e];
+                const int yfac = R.pf[j];
+                int s = -1;
+                for (int t = 0; t < F.nyf; ++t)
+                    if (F.yf[t] == yfac) s = t;
+                if (s < 0) {
+                    if (F.nyf >= NY) return false;
+                    s = F.nyf++;
+                    F.yf[s] = yfac;
+                }
+                F.pyf[np] = s;
+                F.px[np] = R.px[j];
+                F.pg[np] = g;
+                const double c = R.ec[g][e];
+                if (!lead_done[g] && c != 0.0) {
+                    F.plead[np] = 1;
+                    F.pc[np] = 1.0;
+                    F.gs[g] = c;
+                    lead_done[g] = true;
+                } else {
+                    F.plead[np] = 0;
+                    F.pc[np] = lead_done[g] ? c / F.gs[g] : 0.0;
+                }
+                ++np;
+            }
+            if (!lead_done[g]) F.gs[g] = 0.0;
+        }
+        F.np = np;
+        out->push_back(F);
+    }
+    return !out->empty() && (int)out->size() <= f2::kMaxRounds2;
+}
+
+// shape of the fused-v2 round tables per part
+constexpr int kSX = 4, kSP = 9, kSG = 4, kSY = 4;  // stiffness part
+constexpr int kMX = 1, kMP = 1, kMG = 1, kMY = 1;  // mass part
+
+template <int P>
+constexpr int rows_per_thread() {
+    return P == 3 ? 32 : (P == 4 ? 24 : (P == 2 ? 32 : 16));
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale, int accumulate,
+                    int batch, cudaStream_t st) {
+    using namespace f2;
+    Args2 a;
+    memset(&a, 0, sizeof a);
+    a.src = src;
+    a.dst = dst;
+    a.scale = scale;
+    a.accumulate = accumulate;
+    a.bx = op->F[0].band;
+    a.by = op->F[1].band;
+    a.bz = op->F[2].band;
+    a.rounds = pl.d_f2;
+    a.nrounds = (int)pl.f2_nrounds;
+    a.mx = op->m[0];
+    a.my = op->m[1];
+    a.mz = op->m[2];
+    a.batch = batch;
+    a.tiles_x = (a.mx + TX - 1) / TX;
+    a.tiles_y = (a.my + L - 1) / L;
+    a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // persistent CTAs (one per SM); keep segments >= 2P+2 planes and <= 3 mz units per CTA
+    long long nct = sms;
+    const long long minlen = 2 * P + 2;
+    if (a.units / nct < minlen) nct = a.units / minlen;
+    if (nct < 1) nct = 1;
+    while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
+    a.nctas = (int)nct;
+    const size_t sm = smem_bytes<P, L, NX, NP, NG, NY>(a.nrounds);
+    auto kern = k_fused2<P, L, NX, NP, NG, NY>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * L * TX;
+    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    if (e) return e;
+    kern<<<a.nctas, NW * 32, sm, st>>>(a);
+    e = cudaGetLastError();
+    if (!e) {
+        const long long tot = (long long)a.tiles_x * a.tiles_y * batch * a.mz * L * TX;
+        long long nb = (tot + 255) / 256;
+        k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, L);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(a.scratch, st);
+    return e;
+}
+
+template <int P>
+cudaError_t launch_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                        int accumulate, int batch, cudaStream_t st) {
+    constexpr int L = rows_per_thread<P>();
+    if (part == 0) return launch2<P, L, kMX, kMP, kMG, kMY>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch2<P, L, kSX, kSP, kSG, kSY>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+
+}  // namespace
+
+bool fused2_supported(const iga_lr_op* op) {
+    if (op->p[0] != op->p[1] || op->p[0] != op->p[2]) return false;
+    return op->p[0] == 3 || op->p[0] == 4;
+}
+
+bool fused2_preferred(const iga_lr_op* op, int batch) {
+    // 128-wide tiles: narrow meshes waste lanes; small meshes cannot fill the persistent grid
+    const long long N = (long long)op->m[0] * op->m[1] * op->m[2] * batch;
+    return op->m[0] >= 96 && N >= (1LL << 21);
+}
+
+iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part) {
+    if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
+    size_t bytes = 0;
+    std::vector<char> blob;
+    if (part == 0) {
+        std::vector<f2::Round2<kMX, kMP, kMG>> v;
+        if (!build_rounds2<kMX, kMP, kMG, kMY>(*pl, &v)) return IGA_EUNSUPPORTED;
+        bytes = sizeof(v[0]) * v.size();
+        blob.assign((const char*)v.data(), (const char*)v.data() + bytes);
+        pl->f2_nrounds = (int)v.size();
+    } else {
+        std::vector<f2::Round2<kSX, kSP, kSG>> v;
+        if (!build_rounds2<kSX, kSP, kSG, kSY>(*pl, &v)) return IGA_EUNSUPPORTED;
+        bytes = sizeof(v[0]) * v.size();
+        blob.assign((const char*)v.data(), (const char*)v.data() + bytes);
+        pl->f2_nrounds = (int)v.size();
+    }
+    // shared memory budget
+    size_t sm = 0;
+    if (op->p[0] == 3)
+        sm = part ? f2::smem_bytes<3, rows_per_thread<3>(), kSX, kSP, kSG, kSY>(pl->f2_nrounds)
+                  : f2::smem_bytes<3, rows_per_thread<3>(), kMX, kMP, kMG, kMY>(pl->f2_nrounds);
+    else
+        sm = part ? f2::smem_bytes<4, rows_per_thread<4>(), kSX, kSP, kSG, kSY>(pl->f2_nrounds)
+                  : f2::smem_bytes<4, rows_per_thread<4>(), kMX, kMP, kMG, kMY>(pl->f2_nrounds);
+    if (sm > 227 * 1024) return IGA_EUNSUPPORTED;
+    cudaError_t e = cudaMalloc(&pl->d_f2, bytes);
+    if (e) return cuda_error(e, "cudaMalloc(f2 rounds)");
+    e = cudaMemcpy(pl->d_f2, blob.data(), bytes, cudaMemcpyHostToDevice);
+    if (e) return cuda_error(e, "f2 rounds H2D");
+    pl->f2_ok = true;
+    return IGA_OK;
+}
+
+iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                             int accumulate, int batch, cudaStream_t st) {
+    cudaError_t e = cudaErrorInvalidValue;
+    if (op->p[0] == 3) e = launch_part<3>(op, pl, part, src, dst, scale, accumulate, batch, st);
+    else if (op->p[0] == 4) e = launch_part<4>(op, pl, part, src, dst, scale, accumulate, batch, st);
+    if (e) return cuda_error(e, "k_fused2");
+    return IGA_OK;
+}
+
+}  // namespace igalr

@@ -63,8 +63,15 @@ struct Plan {
     int n_x = 0, n_y = 0, n_z = 0;  // mode products per vector
     double flops = 0;               // algorithmic flops per vector (2 * nnz per mode product)
     bool fused_ok = false;
+    void* d_fused = nullptr;        // device copy of the fused kernel's round tables
+    int fused_nslot = 1;            // input slots used by the plan
+    int fused_parts = 1;            // 1 or 2 output parts
+    int fused_part = 0;             // the part when fused_parts == 1
+    void* d_f2 = nullptr;           // fused-v2 round tables (single-part plans only)
+    int f2_nrounds = 0;
+    bool f2_ok = false;
 };
-enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kNumPlans = 4 };
+enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kPlanF2Mass = 4, kPlanF2Stiff = 5, kNumPlans = 6 };
 }  // namespace igalr
 
 struct iga_lr_op {
@@ -103,6 +110,13 @@ iga_status assemble_dir(const DirQuad& q, const std::vector<std::vector<double>>
 iga_status apply_unfused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
 iga_status apply_fused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
 bool fused_supported(const iga_lr_op* op, const Plan& pl);
+iga_status prepare_fused(const iga_lr_op* op, Plan* pl);
+void release_fused(Plan* pl);
+bool fused2_supported(const iga_lr_op* op);
+bool fused2_preferred(const iga_lr_op* op, int batch);
+iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part);
+iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                             int accumulate, int batch, cudaStream_t st);
 iga_status kkt_combos(const double* in, double* abc, int n_t, int64_t N, double tau, double beta,
                       cudaStream_t st);
 

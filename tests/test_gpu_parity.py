@@ -52,7 +52,7 @@ def sample_rows(dims, count, seed, p):
     return np.unique(np.array(rows, dtype=np.int64))
 
 
-PATHS = ["unfused", "auto"]
+PATHS = ["unfused", "fused_v1", "fused", "auto"]
 
 
 # ----------------------------------------------------------------------------- factors
@@ -221,6 +221,10 @@ def test_edge_shapes(env, path, p, n, nq, dirichlet):
     m = n - 2 if dirichlet else n
     x = np.random.default_rng(1).standard_normal((2, m, m, m))
     M, S = oracle.assemble_csr(P)
+    if path == "fused_v1" and not op.info_dict()["fused_ok"]:
+        pytest.skip("first-generation fused kernel supports p <= 5 only")
+    if path == "fused" and not (op.info_dict()["fused2_ok"] or op.info_dict()["fused_ok"]):
+        pytest.skip("no fused kernel for this degree")
     yM, yS = gpu_apply(env, op, x, path)
     for b in range(2):
         assert rel(yM[b], oracle.spmv(M, x[b])) <= TOL
