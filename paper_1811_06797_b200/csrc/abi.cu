@@ -1,6 +1,7 @@
 // abi.cu — C ABI of libigalr (include/iga_lr.h): validation, Gauss rule, factor
 // deduplication, the shared-prefix evaluation plan, and dispatch of the CUDA kernels.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -406,10 +407,12 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
         if (op->has_mass) {
             build_plan(op, tm, false, &op->plan[kPlanF2Mass], lm, false);
             if (prepare_fused2(op, &op->plan[kPlanF2Mass], 0) != IGA_OK) op->plan[kPlanF2Mass].f2_ok = false;
+            prepare_canon(op, &op->plan[kPlanF2Mass], 0);
         }
         if (op->has_stiff) {
             build_plan(op, ts, false, &op->plan[kPlanF2Stiff], ls, false);
             if (prepare_fused2(op, &op->plan[kPlanF2Stiff], 1) != IGA_OK) op->plan[kPlanF2Stiff].f2_ok = false;
+            prepare_canon(op, &op->plan[kPlanF2Stiff], 1);
         }
         g_err.clear();
     }
@@ -426,6 +429,7 @@ void iga_lr_destroy(iga_lr_op* op) {
     for (int k = 0; k < kNumPlans; ++k) {
         release_fused(&op->plan[k]);
         if (op->plan[k].d_f2) cudaFree(op->plan[k].d_f2);
+        if (op->plan[k].d_canon) cudaFree(op->plan[k].d_canon);
     }
     delete op;
 }
@@ -453,9 +457,15 @@ static iga_status run_f2(const iga_lr_op* op, const double* xm, const double* xs
     if (need_m && !op->plan[kPlanF2Mass].f2_ok) return IGA_EUNSUPPORTED;
     if (need_s && !op->plan[kPlanF2Stiff].f2_ok) return IGA_EUNSUPPORTED;
     iga_status s = IGA_OK;
-    if (need_m) s = apply_fused2_part(op, op->plan[kPlanF2Mass], 0, xm, dm, alpha, 0, batch, st);
-    if (!s && need_s)
-        s = apply_fused2_part(op, op->plan[kPlanF2Stiff], 1, xs, ds, gamma, (need_m && dm == ds) ? 1 : 0, batch, st);
+    const char* gen = getenv("IGALR_F2_GENERIC");
+    const bool canon_ok = !(gen && gen[0] == '1');
+    auto part_run = [&](int part, const double* x, double* d, double sc, int acc) {
+        const Plan& pl = op->plan[part ? kPlanF2Stiff : kPlanF2Mass];
+        if (canon_ok && pl.canon_ok) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, st);
+        return apply_fused2_part(op, pl, part, x, d, sc, acc, batch, st);
+    };
+    if (need_m) s = part_run(0, xm, dm, alpha, 0);
+    if (!s && need_s) s = part_run(1, xs, ds, gamma, (need_m && dm == ds) ? 1 : 0);
     return s;
 }
 

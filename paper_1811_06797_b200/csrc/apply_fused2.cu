@@ -17,6 +17,7 @@
 // Planes whose inputs span two CTAs' ranges are written to per-CTA scratch and summed by
 // k_fixup in CTA order (deterministic; no atomics).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -433,6 +434,330 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fused2(const Args2 a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
 }
 
+// ------------------------------------------------------------------------------------
+// Canonical round shapes: the plan structure is compile-time, only factor ids and the
+// pair/group coefficients are runtime data.  Stiffness (reading A of G6): for
+// every r the 9 blocks q_kl share v_r, giving x-entries [K,E,T,M] (patterns (1,1),(0,1),
+// (1,0),(0,0)), y-factors [M,T,E,K], z-groups [M,T,E,K] and the 9 (y,x)->z pairs below.
+struct ShapeStiffA {
+    static constexpr int NX = 4, NY = 4, NG = 4, NPAIR = 9;
+    __host__ __device__ static constexpr int px(int j) { return j == 0 ? 0 : (j <= 2 ? 1 : (j == 3 || j == 6) ? 2 : 3); }
+    __host__ __device__ static constexpr int py(int j) {
+        return (j == 0 || j == 2 || j == 6 || j == 8) ? 0 : (j == 1 || j == 7) ? 1 : (j == 3 || j == 5) ? 2 : 3;
+    }
+    __host__ __device__ static constexpr int pg(int j) {
+        return (j == 0 || j == 1 || j == 3 || j == 4) ? 0 : (j == 2 || j == 5) ? 1 : (j == 6 || j == 7) ? 2 : 3;
+    }
+    __host__ __device__ static constexpr bool lead(int j) { return j == 0 || j == 2 || j == 6 || j == 8; }
+};
+struct ShapeMass {
+    static constexpr int NX = 1, NY = 1, NG = 1, NPAIR = 1;
+    __host__ __device__ static constexpr int px(int) { return 0; }
+    __host__ __device__ static constexpr int py(int) { return 0; }
+    __host__ __device__ static constexpr int pg(int) { return 0; }
+    __host__ __device__ static constexpr bool lead(int) { return true; }
+};
+
+template <class S>
+struct RoundC {
+    int xf[S::NX], yf[S::NY], gf[S::NG];
+    int pad;
+    double pc[S::NPAIR];   // coefficient ratio of non-lead pairs
+    double gs[S::NG];      // group scale (lead pair coefficient)
+};
+
+template <int P, int TY>
+struct GeoC {
+    static constexpr int BW = 2 * P + 1;
+    static constexpr int BWP = (BW + 1) & ~1;     // y-coef row pitch (16-byte aligned rows)
+    static constexpr int HY = TY + 2 * P;
+    static constexpr int HX = TX + 2 * P;
+    static constexpr int HXP = HX + 1;
+};
+
+template <class S, int P, int LW, int WPQ>
+__global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
+    constexpr int TY = LW * WPQ;
+    using G_ = GeoC<P, TY>;
+    constexpr int BW = G_::BW, BWP = G_::BWP, HY = G_::HY, HXP = G_::HXP;
+    constexpr int NX = S::NX, NY = S::NY, NG = S::NG, NPAIR = S::NPAIR;
+    using RS = RingShape<BW>;
+    using RoundT = RoundC<S>;
+    static_assert(LW * RS::COLS * WPQ <= 512, "ring does not fit in TMEM");
+
+    extern __shared__ __align__(16) double sm[];
+    double* vin = sm;                                   // [2][HY][HXP]
+    double* xcs = vin + 2 * HY * HXP;                   // [2][NX][TX][BW]
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nrounds][NY][TY][BWP]
+    double* zcs = ycs + (size_t)a.nrounds * NY * TY * BWP;  // [2][nrounds][NG][BW]
+    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int quad = warp & 3, sub = warp >> 2;
+    const int cx = quad * TXW + lane;  // tile column of this thread
+    const int row0 = sub * LW;         // first tile output row of this warp
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < a.nrounds * (int)(sizeof(RoundT) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(rs)[i] = reinterpret_cast<const int*>(a.rounds)[i];
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sub * (512 / WPQ));
+
+    const long long plane = (long long)a.mx * a.my;
+    const long long u0 = unit_begin(blockIdx.x, a.units, a.nctas);
+    const long long u1 = unit_begin(blockIdx.x + 1, a.units, a.nctas);
+
+    int seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / a.mz;
+        const int za = (int)(u - tile * a.mz);
+        const int zb = (int)min((long long)a.mz, (long long)za + (u1 - u));
+        u += zb - za;
+        long long tt = tile;
+        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+        const int b = (int)tt;
+        const int x0 = txi * TX, y0 = tyi * TY;
+        const long long vb = (long long)b * a.mz * plane;
+        const int gx = x0 + cx;
+
+        __syncthreads();
+        for (int r = 0; r < a.nrounds; ++r) {
+            const RoundT& R = rs[r];
+            for (int i = threadIdx.x; i < NY * TY * BWP; i += blockDim.x) {
+                const int s = i / (TY * BWP), rem = i - s * TY * BWP;
+                const int row = rem / BWP, k = rem - row * BWP;
+                const int gy = y0 + row;
+                const bool ok = gy < a.my && k < BW;
+                cp8(ycs + (size_t)r * NY * TY * BWP + i, ok ? a.by + ((size_t)R.yf[s] * a.my + gy) * BW + k : a.by, ok);
+            }
+        }
+        {
+            double zero[RS::DBL];
+#pragma unroll
+            for (int k = 0; k < RS::DBL; ++k) zero[k] = 0.0;
+            for (int i = 0; i < LW; ++i) ring_st<BW>(tbase + i * RS::COLS, zero);
+        }
+
+        auto stage_plane = [&](int zp, int buf) {
+            double* dstp = vin + buf * HY * HXP;
+            const double* srcp = a.src + vb + (long long)zp * plane;
+            for (int i = threadIdx.x; i < HY * G_::HX; i += blockDim.x) {
+                const int r = i / G_::HX, c = i - r * G_::HX;
+                const int gy = y0 - P + r, gxx = x0 - P + c;
+                const bool ok = gy >= 0 && gy < a.my && gxx >= 0 && gxx < a.mx;
+                cp8(dstp + r * HXP + c, ok ? srcp + (long long)gy * a.mx + gxx : a.src, ok);
+            }
+            double* zdst = zcs + buf * a.nrounds * NG * BW;
+            for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
+                const int r = i / (NG * BW), rem = i - r * NG * BW;
+                const int g = rem / BW, j = rem - g * BW;
+                const RoundT& R = rs[r];
+                const int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;
+                const bool ok = zo >= 0 && zo < a.mz;
+                cp8(zdst + i, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
+            }
+        };
+        auto stage_xc = [&](int r, int buf) {
+            const RoundT& R = rs[r];
+            double* dstp = xcs + buf * NX * TX * BW;
+            for (int i = threadIdx.x; i < NX * TX * BW; i += blockDim.x) {
+                const int e = i / (TX * BW), rem = i - e * TX * BW;
+                const int c = rem / BW, k = rem - c * BW;
+                const int g = x0 + c;
+                const bool ok = g < a.mx;
+                cp8(dstp + i, ok ? a.bx + ((size_t)R.xf[e] * a.mx + g) * BW + k : a.bx, ok);
+            }
+        };
+
+        stage_plane(za, 0);
+        stage_xc(0, 0);
+        cp_commit();
+        int pbuf = 0, xbuf = 0;
+        for (int zp = za; zp < zb; ++zp) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                const bool last_round = (r == a.nrounds - 1);
+                cp_wait<0>();
+                tm_wait_st();
+                __syncthreads();
+                if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                if (r == 0 && zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
+                cp_commit();
+
+                const RoundT& R = rs[r];
+                const double* vt = vin + pbuf * HY * HXP + row0 * HXP + cx;
+                const double* xc = xcs + xbuf * NX * TX * BW;
+                const double* yc = ycs + (size_t)r * NY * TY * BWP + (size_t)row0 * BWP;
+                const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
+                double xr[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) xr[e][k] = xc[(e * TX + cx) * BW + k];
+                double zr[NG][BW];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    const double gsc = R.gs[g];
+#pragma unroll
+                    for (int j = 0; j < BW; ++j) zr[g][j] = zc[g * BW + j] * gsc;
+                }
+                double pc[NPAIR];
+#pragma unroll
+                for (int j = 0; j < NPAIR; ++j) pc[j] = R.pc[j];
+                const int zret = zp - P;
+                const int jret = ((zret % BW) + BW) % BW;
+                bool ret_valid = false, ret_complete = false;
+                if (last_round && zret >= 0 && zret < a.mz) {
+                    ret_valid = true;
+                    const int lo = max(0, zret - P), hi = min(a.mz - 1, zret + P);
+                    ret_complete = lo >= za && hi <= zb - 1;
+                }
+
+                double w[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) w[e][k] = 0.0;
+
+#pragma unroll 1
+                for (int base = 0; base < LW + 2 * P; base += BW) {
+#pragma unroll
+                    for (int q = 0; q < BW; ++q) {
+                        const int step = base + q;
+                        if (step < LW + 2 * P) {
+                            double v[BW];
+#pragma unroll
+                            for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
+#pragma unroll
+                            for (int e = 0; e < NX; ++e) {
+                                double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                                for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
+#pragma unroll
+                                for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
+                                w[e][q] = acc0 + acc1;
+                            }
+                            if (step >= 2 * P) {
+                                const int i = step - 2 * P;
+                                const uint32_t tp = tbase + i * RS::COLS;
+                                double ring[RS::DBL];
+                                ring_ld<BW>(tp, ring);
+                                double G[NG];
+#pragma unroll
+                                for (int g = 0; g < NG; ++g) G[g] = 0.0;
+                                const double* ycr = yc + (size_t)i * BWP;
+#pragma unroll
+                                for (int f = 0; f < NY; ++f) {
+                                    double yv[BWP];
+                                    const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
+#pragma unroll
+                                    for (int k = 0; k < BWP / 2; ++k) {
+                                        const double2 t2 = y2[k];
+                                        yv[2 * k] = t2.x;
+                                        yv[2 * k + 1] = t2.y;
+                                    }
+#pragma unroll
+                                    for (int j = 0; j < NPAIR; ++j) {
+                                        if (S::py(j) != f) continue;
+                                        constexpr int dummy = 0;
+                                        (void)dummy;
+                                        const int e = S::px(j);
+                                        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+                                        for (int k = 0; k < BW; k += 2) u0 = fma(yv[k], w[e][(q + 1 + k) % BW], u0);
+#pragma unroll
+                                        for (int k = 1; k < BW; k += 2) u1 = fma(yv[k], w[e][(q + 1 + k) % BW], u1);
+                                        const int g = S::pg(j);
+                                        if (S::lead(j)) G[g] += u0 + u1;
+                                        else G[g] = fma(pc[j], u0 + u1, G[g]);
+                                    }
+                                }
+#pragma unroll
+                                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                                if (ret_valid) {
+                                    double val = 0.0;
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j)
+                                        if (j == jret) {
+                                            val = ring[j];
+                                            ring[j] = 0.0;
+                                        }
+                                    const int gy = y0 + row0 + i;
+                                    if (gy < a.my && gx < a.mx) {
+                                        if (ret_complete) {
+                                            const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                            a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                        } else {
+                                            const int slot = partial_slot(zret, za, zb, P);
+                                            a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                                                a.scale * val;
+                                        }
+                                    }
+                                }
+                                ring_st<BW>(tp, ring);
+                            }
+                        }
+                    }
+                }
+                if (last_round) pbuf ^= 1;
+                xbuf ^= 1;
+            }
+        }
+        tm_wait_st();
+        __syncthreads();
+        for (int i = 0; i < LW; ++i) {
+            const uint32_t tp = tbase + i * RS::COLS;
+            double ring[RS::DBL];
+            ring_ld<BW>(tp, ring);
+            const int gy = y0 + row0 + i;
+#pragma unroll
+            for (int s = 0; s < 2 * P; ++s) {
+                const int zo = zb - P + s;
+                if (zo < 0 || zo >= a.mz) continue;
+                const int j = zo % BW;
+                double val = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BW; ++jj)
+                    if (jj == j) val = ring[jj];
+                if (gy < a.my && gx < a.mx) {
+                    const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+                    const bool complete = lo >= za && hi <= zb - 1;
+                    if (complete) {
+                        const long long o = vb + (long long)zo * plane + (long long)gy * a.mx + gx;
+                        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                    } else {
+                        const int slot = partial_slot(zo, za, zb, P);
+                        a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                            a.scale * val;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
+}
+
+template <class S, int P, int LW, int WPQ>
+size_t smem_bytes_canon(int nrounds) {
+    constexpr int TY = LW * WPQ;
+    using G_ = GeoC<P, TY>;
+    return sizeof(double) * (2 * G_::HY * G_::HXP + 2 * S::NX * TX * G_::BW + (size_t)nrounds * S::NY * TY * G_::BWP +
+                             2 * (size_t)nrounds * S::NG * G_::BW) +
+           sizeof(RoundC<S>) * nrounds + 64;
+}
+
 // Sum partial planes: for every (tile, zo) whose inputs span several CTA ranges, add the
 // contributions of those CTAs in increasing CTA order.
 __global__ void k_fixup(const Args2 a, int P, int L) {
@@ -620,6 +945,194 @@ cudaError_t launch_part(const iga_lr_op* op, const Plan& pl, int part, const dou
     return launch2<P, L, kSX, kSP, kSG, kSY>(op, pl, src, dst, scale, accumulate, batch, st);
 }
 
+
+// ---- canonical-shape host side
+template <class S>
+bool build_canon(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<S>>* out);
+
+template <>
+bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMass>>* out) {
+    (void)op;
+    out->clear();
+    for (const Round& R : pl.rounds) {
+        if (R.nx != 1 || R.np != 1 || R.ng != 1 || R.ne[0] != 1) return false;
+        f2::RoundC<f2::ShapeMass> C;
+        memset(&C, 0, sizeof C);
+        C.xf[0] = R.xf[0];
+        C.yf[0] = R.pf[0];
+        C.gf[0] = R.gf[0];
+        C.gs[0] = R.ec[0][0];
+        C.pc[0] = 1.0;
+        out->push_back(C);
+    }
+    return !out->empty() && out->size() <= (size_t)f2::kMaxRounds2;
+}
+
+template <>
+bool build_canon<f2::ShapeStiffA>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeStiffA>>* out) {
+    using S = f2::ShapeStiffA;
+    out->clear();
+    // pattern (a*2+b) -> canonical slot; x: [K,E,T,M], y and z: [M,T,E,K]
+    auto xslot = [](int pat) { return pat == 3 ? 0 : pat == 1 ? 1 : pat == 2 ? 2 : 3; };
+    auto yslot = [](int pat) { return pat == 0 ? 0 : pat == 2 ? 1 : pat == 1 ? 2 : 3; };
+    for (const Round& R : pl.rounds) {
+        f2::RoundC<S> C;
+        memset(&C, 0, sizeof C);
+        int xs[4] = {-1, -1, -1, -1}, ys[4] = {-1, -1, -1, -1}, gsl[4] = {-1, -1, -1, -1};
+        for (int e = 0; e < R.nx; ++e) {
+            const int s = xslot(op->F[0].pattern[R.xf[e]]);
+            if (xs[s] >= 0) return false;
+            xs[s] = R.xf[e];
+        }
+        for (int g = 0; g < R.ng; ++g) {
+            const int s = yslot(op->F[2].pattern[R.gf[g]]);
+            if (gsl[s] >= 0) return false;
+            gsl[s] = R.gf[g];
+        }
+        double cj[S::NPAIR];
+        bool seen[S::NPAIR] = {};
+        for (int g = 0; g < R.ng; ++g) {
+            const int gs_ = yslot(op->F[2].pattern[R.gf[g]]);
+            for (int e = 0; e < R.ne[g]; ++e) {
+                const int j = R.ep[g][e];
+                const int xsl = xslot(op->F[0].pattern[R.xf[R.px[j]]]);
+                const int ysl = yslot(op->F[1].pattern[R.pf[j]]);
+                if (ys[ysl] >= 0 && ys[ysl] != R.pf[j]) return false;
+                ys[ysl] = R.pf[j];
+                int cj_idx = -1;
+                for (int k = 0; k < S::NPAIR; ++k)
+                    if (S::px(k) == xsl && S::py(k) == ysl && S::pg(k) == gs_) cj_idx = k;
+                if (cj_idx < 0 || seen[cj_idx]) return false;
+                seen[cj_idx] = true;
+                cj[cj_idx] = R.ec[g][e];
+            }
+        }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (!seen[k]) return false;
+        for (int s = 0; s < 4; ++s)
+            if (xs[s] < 0 || ys[s] < 0 || gsl[s] < 0) return false;
+        for (int s = 0; s < 4; ++s) {
+            C.xf[s] = xs[s];
+            C.yf[s] = ys[s];
+            C.gf[s] = gsl[s];
+        }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (S::lead(k)) {
+                if (cj[k] == 0.0) return false;
+                C.gs[S::pg(k)] = cj[k];
+                C.pc[k] = 1.0;
+            }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (!S::lead(k)) C.pc[k] = cj[k] / C.gs[S::pg(k)];
+        out->push_back(C);
+    }
+    return !out->empty() && out->size() <= (size_t)f2::kMaxRounds2;
+}
+
+static int env_wpq() {
+    const char* s = getenv("IGALR_WPQ");
+    return (s && s[0] == '1') ? 1 : 2;
+}
+
+template <class S, int P, int LW, int WPQ>
+cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                           int accumulate, int batch, cudaStream_t st) {
+    using namespace f2;
+    constexpr int TY = LW * WPQ;
+    Args2 a;
+    memset(&a, 0, sizeof a);
+    a.src = src;
+    a.dst = dst;
+    a.scale = scale;
+    a.accumulate = accumulate;
+    a.bx = op->F[0].band;
+    a.by = op->F[1].band;
+    a.bz = op->F[2].band;
+    a.rounds = pl.d_canon;
+    a.nrounds = pl.canon_nrounds;
+    a.mx = op->m[0];
+    a.my = op->m[1];
+    a.mz = op->m[2];
+    a.batch = batch;
+    a.tiles_x = (a.mx + TX - 1) / TX;
+    a.tiles_y = (a.my + TY - 1) / TY;
+    a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long nct = sms;
+    const long long minlen = 2 * P + 2;
+    if (a.units / nct < minlen) nct = a.units / minlen;
+    if (nct < 1) nct = 1;
+    while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
+    a.nctas = (int)nct;
+    const size_t sm = smem_bytes_canon<S, P, LW, WPQ>(a.nrounds);
+    auto kern = k_canon<S, P, LW, WPQ>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TY * TX;
+    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    if (e) return e;
+    kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a);
+    e = cudaGetLastError();
+    if (!e) {
+        const long long tot = (long long)a.tiles_x * a.tiles_y * batch * a.mz * TY * TX;
+        long long nb = (tot + 255) / 256;
+        k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, TY);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(a.scratch, st);
+    return e;
+}
+
+template <class S>
+size_t canon_smem(int p, int wpq, int nrounds) {
+    if (p == 3) return wpq == 1 ? f2::smem_bytes_canon<S, 3, 32, 1>(nrounds) : f2::smem_bytes_canon<S, 3, 16, 2>(nrounds);
+    return wpq == 1 ? f2::smem_bytes_canon<S, 4, 24, 1>(nrounds) : f2::smem_bytes_canon<S, 4, 12, 2>(nrounds);
+}
+
+template <class S>
+cudaError_t launch_canon(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                         int accumulate, int batch, cudaStream_t st) {
+    const int wpq = env_wpq();
+    if (op->p[0] == 3)
+        return wpq == 1 ? launch_canon_t<S, 3, 32, 1>(op, pl, src, dst, scale, accumulate, batch, st)
+                        : launch_canon_t<S, 3, 16, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+    return wpq == 1 ? launch_canon_t<S, 4, 24, 1>(op, pl, src, dst, scale, accumulate, batch, st)
+                    : launch_canon_t<S, 4, 12, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+
+template <class S>
+iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
+    std::vector<f2::RoundC<S>> v;
+    if (!build_canon<S>(op, *pl, &v)) return IGA_EUNSUPPORTED;
+    const int n = (int)v.size();
+    if (canon_smem<S>(op->p[0], 1, n) > 227 * 1024 || canon_smem<S>(op->p[0], 2, n) > 227 * 1024) return IGA_EUNSUPPORTED;
+    cudaError_t e = cudaMalloc(&pl->d_canon, sizeof(v[0]) * n);
+    if (e) return cuda_error(e, "cudaMalloc(canon rounds)");
+    e = cudaMemcpy(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice);
+    if (e) return cuda_error(e, "canon rounds H2D");
+    pl->canon_nrounds = n;
+    pl->canon_ok = true;
+    return IGA_OK;
+}
+
+}  // namespace
+
+iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part) {
+    if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
+    return part == 0 ? prepare_canon_t<f2::ShapeMass>(op, pl) : prepare_canon_t<f2::ShapeStiffA>(op, pl);
+}
+
+iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                            int accumulate, int batch, cudaStream_t st) {
+    cudaError_t e = part == 0 ? launch_canon<f2::ShapeMass>(op, pl, src, dst, scale, accumulate, batch, st)
+                              : launch_canon<f2::ShapeStiffA>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (e) return cuda_error(e, "k_canon");
+    return IGA_OK;
+}
+
+namespace {
 }  // namespace
 
 bool fused2_supported(const iga_lr_op* op) {

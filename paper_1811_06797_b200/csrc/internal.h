@@ -70,6 +70,9 @@ struct Plan {
     void* d_f2 = nullptr;           // fused-v2 round tables (single-part plans only)
     int f2_nrounds = 0;
     bool f2_ok = false;
+    void* d_canon = nullptr;        // canonical-shape round tables (apply_fused2.cu)
+    int canon_nrounds = 0;
+    bool canon_ok = false;
 };
 enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kPlanF2Mass = 4, kPlanF2Stiff = 5, kNumPlans = 6 };
 }  // namespace igalr
@@ -115,6 +118,9 @@ void release_fused(Plan* pl);
 bool fused2_supported(const iga_lr_op* op);
 bool fused2_preferred(const iga_lr_op* op, int batch);
 iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part);
+iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part);
+iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                            int accumulate, int batch, cudaStream_t st);
 iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st);
 iga_status kkt_combos(const double* in, double* abc, int n_t, int64_t N, double tau, double beta,
