@@ -85,7 +85,11 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, double* v) {
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // the wait "modifies" the destination registers so no use can be scheduled before it
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
 }
@@ -107,13 +111,23 @@ __device__ __forceinline__ void tm_ld4(uint32_t taddr, double* v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]));
     v[0] = __hiloint2double(r[1], r[0]);
     v[1] = __hiloint2double(r[3], r[2]);
 }
 __device__ __forceinline__ void tm_st4(uint32_t taddr, const double* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__double2loint(v[0])),
                  "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])));
+}
+__device__ __forceinline__ double tm_ld1(uint32_t taddr) {
+    uint32_t lo, hi;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(lo), "+r"(hi));
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__double2loint(v)),
+                 "r"(__double2hiint(v)));
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -450,13 +464,17 @@ struct ShapeStiffA {
     }
     __host__ __device__ static constexpr bool lead(int j) { return j == 0 || j == 2 || j == 6 || j == 8; }
 };
-struct ShapeMass {
-    static constexpr int NX = 1, NY = 1, NG = 1, NPAIR = 1;
-    __host__ __device__ static constexpr int px(int) { return 0; }
-    __host__ __device__ static constexpr int py(int) { return 0; }
-    __host__ __device__ static constexpr int pg(int) { return 0; }
+// Mass: K consecutive rank-one terms per sweep (independent pipelines sharing the input
+// loads and the ring).
+template <int K>
+struct ShapeMassK {
+    static constexpr int NX = K, NY = K, NG = K, NPAIR = K;
+    __host__ __device__ static constexpr int px(int j) { return j; }
+    __host__ __device__ static constexpr int py(int j) { return j; }
+    __host__ __device__ static constexpr int pg(int j) { return j; }
     __host__ __device__ static constexpr bool lead(int) { return true; }
 };
+using ShapeMass = ShapeMassK<4>;
 
 template <class S>
 struct RoundC {
@@ -683,27 +701,27 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
                                 for (int g = 0; g < NG; ++g)
 #pragma unroll
                                     for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
-                                if (ret_valid) {
-                                    double val = 0.0;
-#pragma unroll
-                                    for (int j = 0; j < BW; ++j)
-                                        if (j == jret) {
-                                            val = ring[j];
-                                            ring[j] = 0.0;
-                                        }
-                                    const int gy = y0 + row0 + i;
-                                    if (gy < a.my && gx < a.mx) {
-                                        if (ret_complete) {
-                                            const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
-                                            a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
-                                        } else {
-                                            const int slot = partial_slot(zret, za, zb, P);
-                                            a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
-                                                a.scale * val;
-                                        }
-                                    }
-                                }
                                 ring_st<BW>(tp, ring);
+                            }
+                        }
+                    }
+                }
+                if (ret_valid) {
+                    // plane zret is final: write it (or its partial) out and clear its slot
+                    tm_wait_st();
+                    for (int i = 0; i < LW; ++i) {
+                        const uint32_t ts = tbase + i * RS::COLS + 2 * jret;
+                        const double val = tm_ld1(ts);
+                        tm_st1(ts, 0.0);
+                        const int gy = y0 + row0 + i;
+                        if (gy < a.my && gx < a.mx) {
+                            if (ret_complete) {
+                                const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                            } else {
+                                const int slot = partial_slot(zret, za, zb, P);
+                                a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                                    a.scale * val;
                             }
                         }
                     }
@@ -758,17 +776,25 @@ size_t smem_bytes_canon(int nrounds) {
            sizeof(RoundC<S>) * nrounds + 64;
 }
 
-// Sum partial planes: for every (tile, zo) whose inputs span several CTA ranges, add the
-// contributions of those CTAs in increasing CTA order.
+// Sum partial planes.  Only planes within P of a CTA-range boundary inside a tile can have
+// inputs in two CTA ranges (segments are >= 2P+2 planes long, so every such plane belongs to
+// exactly one boundary).  Contributions are added in increasing CTA order (deterministic).
 __global__ void k_fixup(const Args2 a, int P, int L) {
     const long long plane = (long long)a.mx * a.my;
-    const int ntile = a.tiles_x * a.tiles_y * a.batch;
-    const long long total = (long long)ntile * a.mz * L * TX;
+    const long long per_b = 2LL * P * L * TX;
+    const long long total = (long long)(a.nctas > 1 ? a.nctas - 1 : 0) * per_b;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
-        const int cx = (int)(g % TX);
-        const int i = (int)((g / TX) % L);
-        const int zo = (int)((g / ((long long)TX * L)) % a.mz);
-        const long long tile = g / ((long long)TX * L * a.mz);
+        const int kb = 1 + (int)(g / per_b);
+        const long long rem = g - (long long)(kb - 1) * per_b;
+        const int s = (int)(rem / ((long long)L * TX));
+        const int i = (int)((rem / TX) % L);
+        const int cx = (int)(rem % TX);
+        const long long ub = unit_begin(kb, a.units, a.nctas);
+        const long long tile = ub / a.mz;
+        const int zbnd = (int)(ub - tile * a.mz);
+        if (zbnd == 0) continue;  // boundary coincides with a tile start: nothing shared
+        const int zo = zbnd - P + s;
+        if (zo < 0 || zo >= a.mz) continue;
         long long tt = tile;
         const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
         const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
@@ -777,20 +803,16 @@ __global__ void k_fixup(const Args2 a, int P, int L) {
         if (gx >= a.mx || gy >= a.my) continue;
         const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
         const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
-        // CTA owning unit ulo / uhi
         long long k0 = (ulo * a.nctas) / a.units;
         while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
         while (unit_begin(k0 + 1, a.units, a.nctas) <= ulo) ++k0;
         long long k1 = (uhi * a.nctas) / a.units;
         while (k1 > 0 && unit_begin(k1, a.units, a.nctas) > uhi) --k1;
         while (unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
-        if (k0 == k1) continue;  // complete inside one CTA segment: written by k_fused2
-        double s = 0.0;
+        double sum = 0.0;
         for (long long k = k0; k <= k1; ++k) {
-            // segment index of `tile` inside CTA k, and its [za, zb)
             const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
-            int seg = 0;
-            int za = 0, zb = 0;
+            int seg = 0, za = 0, zb = 0;
             bool found = false;
             for (long long u = cu0; u < cu1; ++seg) {
                 const long long t2 = u / a.mz;
@@ -806,10 +828,10 @@ __global__ void k_fixup(const Args2 a, int P, int L) {
             }
             if (!found) continue;
             const int slot = partial_slot(zo, za, zb, P);
-            s += a.scratch[((((size_t)k * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx];
+            sum += a.scratch[((((size_t)k * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx];
         }
         const long long o = (long long)b * a.mz * plane + (long long)zo * plane + (long long)gy * a.mx + gx;
-        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + s;
+        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + sum;
     }
 }
 
@@ -928,9 +950,9 @@ cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, doub
     kern<<<a.nctas, NW * 32, sm, st>>>(a);
     e = cudaGetLastError();
     if (!e) {
-        const long long tot = (long long)a.tiles_x * a.tiles_y * batch * a.mz * L * TX;
+        const long long tot = (long long)(a.nctas - 1) * 2 * P * L * TX;
         long long nb = (tot + 255) / 256;
-        k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, L);
+        if (nb > 0) k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, L);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
@@ -953,19 +975,29 @@ bool build_canon(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<S>>
 template <>
 bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMass>>* out) {
     (void)op;
+    constexpr int K = f2::ShapeMass::NX;
     out->clear();
+    std::vector<const Round*> terms;
     for (const Round& R : pl.rounds) {
         if (R.nx != 1 || R.np != 1 || R.ng != 1 || R.ne[0] != 1) return false;
+        terms.push_back(&R);
+    }
+    if (terms.empty()) return false;
+    for (size_t i = 0; i < terms.size(); i += K) {
         f2::RoundC<f2::ShapeMass> C;
         memset(&C, 0, sizeof C);
-        C.xf[0] = R.xf[0];
-        C.yf[0] = R.pf[0];
-        C.gf[0] = R.gf[0];
-        C.gs[0] = R.ec[0][0];
-        C.pc[0] = 1.0;
+        for (int k = 0; k < K; ++k) {
+            const bool real = i + k < terms.size();
+            const Round& R = *terms[real ? i + k : 0];
+            C.xf[k] = R.xf[0];
+            C.yf[k] = R.pf[0];
+            C.gf[k] = R.gf[0];
+            C.gs[k] = real ? R.ec[0][0] : 0.0;  // padding term contributes exactly zero
+            C.pc[k] = 1.0;
+        }
         out->push_back(C);
     }
-    return !out->empty() && out->size() <= (size_t)f2::kMaxRounds2;
+    return out->size() <= (size_t)f2::kMaxRounds2;
 }
 
 template <>
@@ -1076,9 +1108,9 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a);
     e = cudaGetLastError();
     if (!e) {
-        const long long tot = (long long)a.tiles_x * a.tiles_y * batch * a.mz * TY * TX;
+        const long long tot = (long long)(a.nctas - 1) * 2 * P * TY * TX;
         long long nb = (tot + 255) / 256;
-        k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, TY);
+        if (nb > 0) k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, TY);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
