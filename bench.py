@@ -55,7 +55,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -231,8 +231,8 @@ def cpu_oracle_rate(cfgname: str, seconds: float = 12.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "unfused"])
@@ -297,7 +297,7 @@ def main():
             if other == a.config:
                 continue
             try:
-                r2 = time_workload(other, max(3, a.steps // 2), 3, 1, path=a.path, e2e=False)
+                r2 = time_workload(other, max(3, min(a.steps // 2, 50)), 3, 1, path=a.path, e2e=False)
                 v2 = r2["dof"] / (r2["ms"] * 1e-3) / 1e9
                 ach = r2["flops"] / (r2["ms"] * 1e-3) / 1e12 if r2["flops"] else None
                 extra[other] = {"workload": r2["cfg"].name, "GDoF_s": v2, "ms": r2["ms"],

@@ -373,6 +373,15 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     iga_lr_op* op = new (std::nothrow) iga_lr_op();
     if (!op) return set_error(IGA_ENOMEM, "host allocation failed");
     cudaGetDevice(&op->device);
+    {
+        // Stream-ordered scratch (cudaMallocAsync) must not return memory to the OS between
+        // applies: a release threshold of 0 makes every apply re-map ~100 MB (ms of host time).
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, op->device) == cudaSuccess) {
+            uint64_t thr = ~0ULL;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     op->nq = sp->nq ? sp->nq : 0;
     op->dirichlet = dir;
     op->has_mass = omega != nullptr;

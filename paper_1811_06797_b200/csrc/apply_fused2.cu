@@ -566,11 +566,16 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
         auto stage_plane = [&](int zp, int buf) {
             double* dstp = vin + buf * HY * HXP;
             const double* srcp = a.src + vb + (long long)zp * plane;
-            for (int i = threadIdx.x; i < HY * G_::HX; i += blockDim.x) {
-                const int r = i / G_::HX, c = i - r * G_::HX;
-                const int gy = y0 - P + r, gxx = x0 - P + c;
-                const bool ok = gy >= 0 && gy < a.my && gxx >= 0 && gxx < a.mx;
-                cp8(dstp + r * HXP + c, ok ? srcp + (long long)gy * a.mx + gxx : a.src, ok);
+            // rows by warp, contiguous columns by lane: no per-element division
+            for (int r = warp; r < HY; r += NW * WPQ) {
+                const int gy = y0 - P + r;
+                const bool rowok = gy >= 0 && gy < a.my;
+                const double* srow = srcp + (long long)gy * a.mx + (x0 - P);
+                for (int c = lane; c < G_::HX; c += 32) {
+                    const int gxx = x0 - P + c;
+                    const bool ok = rowok && gxx >= 0 && gxx < a.mx;
+                    cp8(dstp + r * HXP + c, ok ? srow + c : a.src, ok);
+                }
             }
             double* zdst = zcs + buf * a.nrounds * NG * BW;
             for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
@@ -583,14 +588,14 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
             }
         };
         auto stage_xc = [&](int r, int buf) {
+            // each entry's band rows for the tile's 128 columns are one contiguous block
+            // (columns past mx read padding / the next factor and are never used)
             const RoundT& R = rs[r];
             double* dstp = xcs + buf * NX * TX * BW;
-            for (int i = threadIdx.x; i < NX * TX * BW; i += blockDim.x) {
-                const int e = i / (TX * BW), rem = i - e * TX * BW;
-                const int c = rem / BW, k = rem - c * BW;
-                const int g = x0 + c;
-                const bool ok = g < a.mx;
-                cp8(dstp + i, ok ? a.bx + ((size_t)R.xf[e] * a.mx + g) * BW + k : a.bx, ok);
+#pragma unroll
+            for (int e = 0; e < NX; ++e) {
+                const double* src = a.bx + ((size_t)R.xf[e] * a.mx + x0) * BW;
+                for (int i = threadIdx.x; i < TX * BW; i += blockDim.x) cp8(dstp + e * TX * BW + i, src + i, true);
             }
         };
 
@@ -777,60 +782,61 @@ size_t smem_bytes_canon(int nrounds) {
 }
 
 // Sum partial planes.  Only planes within P of a CTA-range boundary inside a tile can have
-// inputs in two CTA ranges (segments are >= 2P+2 planes long, so every such plane belongs to
-// exactly one boundary).  Contributions are added in increasing CTA order (deterministic).
+// inputs in several CTA ranges; one CTA per (boundary, plane offset) finds the contributing
+// CTA segments once (thread 0) and all threads add their scratch entries in increasing CTA
+// order (deterministic).
 __global__ void k_fixup(const Args2 a, int P, int L) {
-    const long long plane = (long long)a.mx * a.my;
-    const long long per_b = 2LL * P * L * TX;
-    const long long total = (long long)(a.nctas > 1 ? a.nctas - 1 : 0) * per_b;
-    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
-        const int kb = 1 + (int)(g / per_b);
-        const long long rem = g - (long long)(kb - 1) * per_b;
-        const int s = (int)(rem / ((long long)L * TX));
-        const int i = (int)((rem / TX) % L);
-        const int cx = (int)(rem % TX);
+    __shared__ int s_valid, s_n, s_b, s_zo, s_txi, s_tyi;
+    __shared__ long long s_off[8];
+    const int kb = 1 + blockIdx.x / (2 * P);
+    const int s = blockIdx.x % (2 * P);
+    if (threadIdx.x == 0) {
+        s_valid = 0;
+        s_n = 0;
         const long long ub = unit_begin(kb, a.units, a.nctas);
         const long long tile = ub / a.mz;
         const int zbnd = (int)(ub - tile * a.mz);
-        if (zbnd == 0) continue;  // boundary coincides with a tile start: nothing shared
         const int zo = zbnd - P + s;
-        if (zo < 0 || zo >= a.mz) continue;
-        long long tt = tile;
-        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
-        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
-        const int b = (int)tt;
-        const int gx = txi * TX + cx, gy = tyi * L + i;
-        if (gx >= a.mx || gy >= a.my) continue;
-        const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
-        const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
-        long long k0 = (ulo * a.nctas) / a.units;
-        while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
-        while (unit_begin(k0 + 1, a.units, a.nctas) <= ulo) ++k0;
-        long long k1 = (uhi * a.nctas) / a.units;
-        while (k1 > 0 && unit_begin(k1, a.units, a.nctas) > uhi) --k1;
-        while (unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
-        double sum = 0.0;
-        for (long long k = k0; k <= k1; ++k) {
-            const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
-            int seg = 0, za = 0, zb = 0;
-            bool found = false;
-            for (long long u = cu0; u < cu1; ++seg) {
-                const long long t2 = u / a.mz;
-                const int sa = (int)(u - t2 * a.mz);
-                const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
-                if (t2 == tile) {
-                    za = sa;
-                    zb = sb;
-                    found = true;
-                    break;
+        if (zbnd != 0 && zo >= 0 && zo < a.mz) {
+            long long tt = tile;
+            s_txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+            s_tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+            s_b = (int)tt;
+            s_zo = zo;
+            const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+            const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
+            long long k0 = kb - 1, k1 = kb;
+            while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
+            while (k1 + 1 < a.nctas && unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
+            for (long long k = k0; k <= k1 && s_n < 8; ++k) {
+                const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
+                int seg = 0;
+                for (long long u = cu0; u < cu1; ++seg) {
+                    const long long t2 = u / a.mz;
+                    const int sa = (int)(u - t2 * a.mz);
+                    const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
+                    if (t2 == tile) {
+                        const int slot = partial_slot(zo, sa, sb, P);
+                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)L * TX;
+                        break;
+                    }
+                    u += sb - sa;
                 }
-                u += sb - sa;
             }
-            if (!found) continue;
-            const int slot = partial_slot(zo, za, zb, P);
-            sum += a.scratch[((((size_t)k * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx];
+            s_valid = 1;
         }
-        const long long o = (long long)b * a.mz * plane + (long long)zo * plane + (long long)gy * a.mx + gx;
+    }
+    __syncthreads();
+    if (!s_valid) return;
+    const long long plane = (long long)a.mx * a.my;
+    const long long obase = (long long)s_b * a.mz * plane + (long long)s_zo * plane;
+    for (int p = threadIdx.x; p < L * TX; p += blockDim.x) {
+        const int i = p / TX, cx = p - i * TX;
+        const int gx = s_txi * TX + cx, gy = s_tyi * L + i;
+        if (gx >= a.mx || gy >= a.my) continue;
+        double sum = 0.0;
+        for (int c = 0; c < s_n; ++c) sum += a.scratch[s_off[c] + p];
+        const long long o = obase + (long long)gy * a.mx + gx;
         a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + sum;
     }
 }
@@ -950,9 +956,7 @@ cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, doub
     kern<<<a.nctas, NW * 32, sm, st>>>(a);
     e = cudaGetLastError();
     if (!e) {
-        const long long tot = (long long)(a.nctas - 1) * 2 * P * L * TX;
-        long long nb = (tot + 255) / 256;
-        if (nb > 0) k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, L);
+        if (a.nctas > 1) k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, L);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
@@ -1108,9 +1112,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a);
     e = cudaGetLastError();
     if (!e) {
-        const long long tot = (long long)(a.nctas - 1) * 2 * P * TY * TX;
-        long long nb = (tot + 255) / 256;
-        if (nb > 0) k_fixup<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(a, P, TY);
+        if (a.nctas > 1) k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, TY);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);

@@ -150,7 +150,9 @@ iga_status assemble_dir(const DirQuad& q, const std::vector<std::vector<double>>
     TRY(cudaMalloc(&d_span, sizeof(int) * q.ne));
     TRY(cudaMalloc(&d_eos, sizeof(int) * n));
     TRY(cudaMalloc(&d_spec, sizeof(SpecDev) * nf));
-    TRY(cudaMalloc(&out->band, sizeof(double) * (size_t)nf * m * bw));
+    // tail padding: fused kernels stage whole 128-column tiles of a factor's band rows
+    TRY(cudaMalloc(&out->band, sizeof(double) * ((size_t)nf * m * bw + 256 * bw)));
+    TRY(cudaMemsetAsync(out->band, 0, sizeof(double) * ((size_t)nf * m * bw + 256 * bw), st));
     TRY(cudaMemcpyAsync(d_knots, q.knots.data(), sizeof(double) * q.knots.size(), cudaMemcpyHostToDevice, st));
     TRY(cudaMemcpyAsync(d_node, q.node.data(), sizeof(double) * nnodes, cudaMemcpyHostToDevice, st));
     TRY(cudaMemcpyAsync(d_wgt, q.wgt.data(), sizeof(double) * nnodes, cudaMemcpyHostToDevice, st));
