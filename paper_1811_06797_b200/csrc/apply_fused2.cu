@@ -18,6 +18,7 @@
 // k_fixup in CTA order (deterministic; no atomics).
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 #include <cstring>
 #include <vector>
 
@@ -156,6 +157,58 @@ __device__ __forceinline__ void ring_st(uint32_t t, const double* v) {
     for (int c = 0; c < RS::N16; ++c) tm_st16(t + c * 16, v + c * 8);
 #pragma unroll
     for (int c = 0; c < RS::N4; ++c) tm_st4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+}
+
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// split TMEM ring load: issue now, wait (tied to the registers) when the values are needed
+template <int BW>
+__device__ __forceinline__ void ring_issue(uint32_t t, uint32_t* r) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) {
+        uint32_t* q = r + c * 16;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+              "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+            : "r"(t + c * 16));
+    }
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) {
+        uint32_t* q = r + RS::N16 * 16 + c * 4;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+                     : "r"(t + RS::N16 * 16 + c * 4));
+    }
+}
+template <int BW>
+__device__ __forceinline__ void ring_wait(uint32_t* r, double* v) {
+    using RS = RingShape<BW>;
+    static_assert(RS::DBL * 2 <= 24, "ring_wait handles up to 24 registers");
+    if constexpr (RS::DBL * 2 == 16) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                       "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                       "+r"(r[15]));
+    } else if constexpr (RS::DBL * 2 == 20) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                       "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                       "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]));
+    } else {
+#pragma unroll
+        for (int k = 0; k < RS::DBL * 2; ++k) asm volatile("" : "+r"(r[k]));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+#pragma unroll
+    for (int k = 0; k < RS::DBL; ++k) v[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
 }
 
 template <int P, int L>
@@ -649,68 +702,86 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
 #pragma unroll
                     for (int k = 0; k < BW; ++k) w[e][k] = 0.0;
 
-#pragma unroll 1
-                for (int base = 0; base < LW + 2 * P; base += BW) {
+                // X stage of sweep row `step` into window slot Q (compile-time)
+                auto xstage = [&](auto Qc, int step) {
+                    constexpr int Q = decltype(Qc)::value;
+                    double v[BW];
 #pragma unroll
-                    for (int q = 0; q < BW; ++q) {
-                        const int step = base + q;
-                        if (step < LW + 2 * P) {
-                            double v[BW];
+                    for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
 #pragma unroll
-                            for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
+                    for (int e = 0; e < NX; ++e) {
+                        double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-                            for (int e = 0; e < NX; ++e) {
-                                double acc0 = 0.0, acc1 = 0.0;
+                        for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
 #pragma unroll
-                                for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
+                        for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
+                        w[e][Q] = acc0 + acc1;
+                    }
+                };
+                // Y + Z stages for output row i (window newest row in slot Q)
+                auto yzstage = [&](auto Qc, int i) {
+                    constexpr int Q = decltype(Qc)::value;
+                    const uint32_t tp = tbase + i * RS::COLS;
+                    uint32_t rr[RS::DBL * 2];
+                    ring_issue<BW>(tp, rr);  // TMEM load in flight during the Y stage
+                    double G[NG];
 #pragma unroll
-                                for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
-                                w[e][q] = acc0 + acc1;
-                            }
-                            if (step >= 2 * P) {
-                                const int i = step - 2 * P;
-                                const uint32_t tp = tbase + i * RS::COLS;
-                                double ring[RS::DBL];
-                                ring_ld<BW>(tp, ring);
-                                double G[NG];
+                    for (int g = 0; g < NG; ++g) G[g] = 0.0;
+                    const double* ycr = yc + (size_t)i * BWP;
 #pragma unroll
-                                for (int g = 0; g < NG; ++g) G[g] = 0.0;
-                                const double* ycr = yc + (size_t)i * BWP;
+                    for (int f = 0; f < NY; ++f) {
+                        double yv[BWP];
+                        const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
 #pragma unroll
-                                for (int f = 0; f < NY; ++f) {
-                                    double yv[BWP];
-                                    const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
+                        for (int k = 0; k < BWP / 2; ++k) {
+                            const double2 t2 = y2[k];
+                            yv[2 * k] = t2.x;
+                            yv[2 * k + 1] = t2.y;
+                        }
 #pragma unroll
-                                    for (int k = 0; k < BWP / 2; ++k) {
-                                        const double2 t2 = y2[k];
-                                        yv[2 * k] = t2.x;
-                                        yv[2 * k + 1] = t2.y;
-                                    }
+                        for (int j = 0; j < NPAIR; ++j) {
+                            if (S::py(j) != f) continue;
+                            const int e = S::px(j);
+                            double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-                                    for (int j = 0; j < NPAIR; ++j) {
-                                        if (S::py(j) != f) continue;
-                                        constexpr int dummy = 0;
-                                        (void)dummy;
-                                        const int e = S::px(j);
-                                        double u0 = 0.0, u1 = 0.0;
+                            for (int k = 0; k < BW; k += 2) u0 = fma(yv[k], w[e][(Q + 1 + k) % BW], u0);
 #pragma unroll
-                                        for (int k = 0; k < BW; k += 2) u0 = fma(yv[k], w[e][(q + 1 + k) % BW], u0);
-#pragma unroll
-                                        for (int k = 1; k < BW; k += 2) u1 = fma(yv[k], w[e][(q + 1 + k) % BW], u1);
-                                        const int g = S::pg(j);
-                                        if (S::lead(j)) G[g] += u0 + u1;
-                                        else G[g] = fma(pc[j], u0 + u1, G[g]);
-                                    }
-                                }
-#pragma unroll
-                                for (int g = 0; g < NG; ++g)
-#pragma unroll
-                                    for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
-                                ring_st<BW>(tp, ring);
-                            }
+                            for (int k = 1; k < BW; k += 2) u1 = fma(yv[k], w[e][(Q + 1 + k) % BW], u1);
+                            const int g = S::pg(j);
+                            if (S::lead(j)) G[g] += u0 + u1;
+                            else G[g] = fma(pc[j], u0 + u1, G[g]);
                         }
                     }
+                    double ring[RS::DBL];
+                    ring_wait<BW>(rr, ring);
+#pragma unroll
+                    for (int g = 0; g < NG; ++g)
+#pragma unroll
+                        for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                    ring_st<BW>(tp, ring);
+                };
+                constexpr int HYW = LW + 2 * P;        // rows swept by this warp
+                constexpr int NFULL = (HYW - BW) / BW;  // full blocks after block 0
+                constexpr int REM = (HYW - BW) % BW;
+                // block 0: the first 2P rows only fill the window
+                static_for<0, BW>([&](auto Qc) {
+                    constexpr int Q = decltype(Qc)::value;
+                    xstage(Qc, Q);
+                    if constexpr (Q >= 2 * P) yzstage(Qc, Q - 2 * P);
+                });
+#pragma unroll 1
+                for (int blk = 1; blk <= NFULL; ++blk) {
+                    static_for<0, BW>([&](auto Qc) {
+                        const int step = blk * BW + decltype(Qc)::value;
+                        xstage(Qc, step);
+                        yzstage(Qc, step - 2 * P);
+                    });
                 }
+                static_for<0, REM>([&](auto Qc) {
+                    const int step = (NFULL + 1) * BW + decltype(Qc)::value;
+                    xstage(Qc, step);
+                    yzstage(Qc, step - 2 * P);
+                });
                 if (ret_valid) {
                     // plane zret is final: write it (or its partial) out and clear its slot
                     tm_wait_st();
