@@ -710,12 +710,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
                     for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
 #pragma unroll
                     for (int e = 0; e < NX; ++e) {
-                        double acc0 = 0.0, acc1 = 0.0;
+                        double acc = xr[e][0] * v[0];
 #pragma unroll
-                        for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
-#pragma unroll
-                        for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
-                        w[e][Q] = acc0 + acc1;
+                        for (int k = 1; k < BW; ++k) acc = fma(xr[e][k], v[k], acc);
+                        w[e][Q] = acc;
                     }
                 };
                 // Y + Z stages for output row i (window newest row in slot Q)
@@ -742,14 +740,17 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
                         for (int j = 0; j < NPAIR; ++j) {
                             if (S::py(j) != f) continue;
                             const int e = S::px(j);
-                            double u0 = 0.0, u1 = 0.0;
-#pragma unroll
-                            for (int k = 0; k < BW; k += 2) u0 = fma(yv[k], w[e][(Q + 1 + k) % BW], u0);
-#pragma unroll
-                            for (int k = 1; k < BW; k += 2) u1 = fma(yv[k], w[e][(Q + 1 + k) % BW], u1);
                             const int g = S::pg(j);
-                            if (S::lead(j)) G[g] += u0 + u1;
-                            else G[g] = fma(pc[j], u0 + u1, G[g]);
+                            if (S::lead(j)) {
+                                // lead pair: accumulate straight into its group value
+#pragma unroll
+                                for (int k = 0; k < BW; ++k) G[g] = fma(yv[k], w[e][(Q + 1 + k) % BW], G[g]);
+                            } else {
+                                double u = yv[0] * w[e][(Q + 1) % BW];
+#pragma unroll
+                                for (int k = 1; k < BW; ++k) u = fma(yv[k], w[e][(Q + 1 + k) % BW], u);
+                                G[g] = fma(pc[j], u, G[g]);
+                            }
                         }
                     }
                     double ring[RS::DBL];
