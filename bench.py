@@ -88,13 +88,14 @@ class ClockSampler:
                 "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(backend: str = "nccl"):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        if not dist.is_initialized():
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -105,13 +106,22 @@ def barrier(ws):
 
 
 def allmax(ws, v: float) -> float:
+    """max over ranks (device tensor under NCCL, host tensor under gloo)."""
     if ws == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def weak_scaling_value(ws: int, dof_per_rank: int, local_total_ms: float, steps: int):
+    """Whole-job throughput: all ranks' DoFs / max-over-ranks time (GDoF/s), and ms/step."""
+    tot_ms = allmax(ws, local_total_ms)
+    ms = tot_ms / steps
+    return ws * dof_per_rank / (ms * 1e-3) / 1e9, ms
 
 
 # ----------------------------------------------------------------------------------- GPU arm

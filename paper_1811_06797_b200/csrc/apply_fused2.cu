@@ -16,6 +16,7 @@
 // A plane is retired inline during the last round once its last input plane is processed.
 // Planes whose inputs span two CTAs' ranges are written to per-CTA scratch and summed by
 // k_fixup in CTA order (deterministic; no atomics).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -61,6 +62,7 @@ struct Args2 {
     int tiles_x, tiles_y;
     long long units;       // tiles * mz
     int nctas;
+    int txt, tyt;          // tile width / height (fixup)
 };
 
 constexpr int NSEG = 4;    // max segments per CTA (checked on the host)
@@ -537,19 +539,21 @@ struct RoundC {
     double gs[S::NG];      // group scale (lead pair coefficient)
 };
 
-template <int P, int TY>
+template <int P, int TXT_, int TY>
 struct GeoC {
     static constexpr int BW = 2 * P + 1;
     static constexpr int BWP = (BW + 1) & ~1;     // y-coef row pitch (16-byte aligned rows)
     static constexpr int HY = TY + 2 * P;
-    static constexpr int HX = TX + 2 * P;
+    static constexpr int HX = TXT_ + 2 * P;
     static constexpr int HXP = HX + 1;
 };
 
-template <class S, int P, int LW, int WPQ>
+// QX of the 4 TMEM lane quadrants tile x (32 columns each); the other 4/QX stack in y.
+template <class S, int P, int LW, int WPQ, int QX, bool YRES>
 __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
-    constexpr int TY = LW * WPQ;
-    using G_ = GeoC<P, TY>;
+    constexpr int TX = 32 * QX;                 // tile columns (shadows the 128-wide default)
+    constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
+    using G_ = GeoC<P, TX, TY>;
     constexpr int BW = G_::BW, BWP = G_::BWP, HY = G_::HY, HXP = G_::HXP;
     constexpr int NX = S::NX, NY = S::NY, NG = S::NG, NPAIR = S::NPAIR;
     using RS = RingShape<BW>;
@@ -558,16 +562,19 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
 
     extern __shared__ __align__(16) double sm[];
     double* vin = sm;                                   // [2][HY][HXP]
-    double* xcs = vin + 2 * HY * HXP;                   // [2][NX][TX][BW]
-    double* ycs = xcs + 2 * NX * TX * BW;               // [nrounds][NY][TY][BWP]
-    double* zcs = ycs + (size_t)a.nrounds * NY * TY * BWP;  // [2][nrounds][NG][BW]
+    double* xcs = vin + 2 * HY * HXP;                   // [2][NX][TX][BW]  (per round)
+    // y-coefficients: all rounds resident per segment (YRES) or double-buffered per round
+    constexpr int YSLOTS = YRES ? 0 : 2;
+    const int nyslots = YRES ? a.nrounds : YSLOTS;
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nyslots][NY][TY][BWP]
+    double* zcs = ycs + (size_t)nyslots * NY * TY * BWP;  // [2][nrounds][NG][BW] (per plane)
     RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int quad = warp & 3, sub = warp >> 2;
-    const int cx = quad * TXW + lane;  // tile column of this thread
-    const int row0 = sub * LW;         // first tile output row of this warp
+    const int cx = (quad % QX) * TXW + lane;                 // tile column of this thread
+    const int row0 = ((quad / QX) * WPQ + sub) * LW;          // first tile output row of this warp
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -599,14 +606,16 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
         const int gx = x0 + cx;
 
         __syncthreads();
-        for (int r = 0; r < a.nrounds; ++r) {
-            const RoundT& R = rs[r];
-            for (int i = threadIdx.x; i < NY * TY * BWP; i += blockDim.x) {
-                const int s = i / (TY * BWP), rem = i - s * TY * BWP;
-                const int row = rem / BWP, k = rem - row * BWP;
-                const int gy = y0 + row;
-                const bool ok = gy < a.my && k < BW;
-                cp8(ycs + (size_t)r * NY * TY * BWP + i, ok ? a.by + ((size_t)R.yf[s] * a.my + gy) * BW + k : a.by, ok);
+        if constexpr (YRES) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                const RoundT& R = rs[r];
+                double* ydst = ycs + (size_t)r * NY * TY * BWP;
+                if (lane < BW) {
+                    for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
+                        const int f = rr / TY, row = rr - f * TY;
+                        cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
+                    }
+                }
             }
         }
         {
@@ -641,14 +650,24 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
             }
         };
         auto stage_xc = [&](int r, int buf) {
-            // each entry's band rows for the tile's 128 columns are one contiguous block
-            // (columns past mx read padding / the next factor and are never used)
+            // each factor's band rows for the tile's columns (rows) are one contiguous block
+            // (entries past mx / my read the band allocation's padding or the next factor and
+            // are never used for an output)
             const RoundT& R = rs[r];
             double* dstp = xcs + buf * NX * TX * BW;
 #pragma unroll
             for (int e = 0; e < NX; ++e) {
                 const double* src = a.bx + ((size_t)R.xf[e] * a.mx + x0) * BW;
                 for (int i = threadIdx.x; i < TX * BW; i += blockDim.x) cp8(dstp + e * TX * BW + i, src + i, true);
+            }
+            // y rows re-pitched from BW to BWP (16-byte aligned) for LDS.128 broadcasts
+            if (YRES) return;
+            double* ydst = ycs + buf * NY * TY * BWP;
+            if (lane < BW) {
+                for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
+                    const int f = rr / TY, row = rr - f * TY;
+                    cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
+                }
             }
         };
 
@@ -670,7 +689,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
                 const RoundT& R = rs[r];
                 const double* vt = vin + pbuf * HY * HXP + row0 * HXP + cx;
                 const double* xc = xcs + xbuf * NX * TX * BW;
-                const double* yc = ycs + (size_t)r * NY * TY * BWP + (size_t)row0 * BWP;
+                const double* yc = ycs + (size_t)(YRES ? r : xbuf) * NY * TY * BWP + (size_t)row0 * BWP;
                 const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
                 double xr[NX][BW];
 #pragma unroll
@@ -731,7 +750,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
                         double yv[BWP];
                         const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
 #pragma unroll
-                        for (int k = 0; k < BWP / 2; ++k) {
+                        for (int k = 0; k < BWP / 2; ++k) {  // broadcast LDS.128
                             const double2 t2 = y2[k];
                             yv[2 * k] = t2.x;
                             yv[2 * k + 1] = t2.y;
@@ -844,11 +863,12 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
 }
 
-template <class S, int P, int LW, int WPQ>
+template <class S, int P, int LW, int WPQ, int QX, bool YRES>
 size_t smem_bytes_canon(int nrounds) {
-    constexpr int TY = LW * WPQ;
-    using G_ = GeoC<P, TY>;
-    return sizeof(double) * (2 * G_::HY * G_::HXP + 2 * S::NX * TX * G_::BW + (size_t)nrounds * S::NY * TY * G_::BWP +
+    constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
+    using G_ = GeoC<P, TXT, TYT>;
+    const size_t ys = YRES ? (size_t)nrounds : 2;
+    return sizeof(double) * (2 * G_::HY * G_::HXP + 2 * S::NX * TXT * G_::BW + ys * S::NY * TYT * G_::BWP +
                              2 * (size_t)nrounds * S::NG * G_::BW) +
            sizeof(RoundC<S>) * nrounds + 64;
 }
@@ -889,7 +909,7 @@ __global__ void k_fixup(const Args2 a, int P, int L) {
                     const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
                     if (t2 == tile) {
                         const int slot = partial_slot(zo, sa, sb, P);
-                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)L * TX;
+                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)a.tyt * a.txt;
                         break;
                     }
                     u += sb - sa;
@@ -902,9 +922,9 @@ __global__ void k_fixup(const Args2 a, int P, int L) {
     if (!s_valid) return;
     const long long plane = (long long)a.mx * a.my;
     const long long obase = (long long)s_b * a.mz * plane + (long long)s_zo * plane;
-    for (int p = threadIdx.x; p < L * TX; p += blockDim.x) {
-        const int i = p / TX, cx = p - i * TX;
-        const int gx = s_txi * TX + cx, gy = s_tyi * L + i;
+    for (int p = threadIdx.x; p < a.tyt * a.txt; p += blockDim.x) {
+        const int i = p / a.txt, cx = p - i * a.txt;
+        const int gx = s_txi * a.txt + cx, gy = s_tyi * a.tyt + i;
         if (gx >= a.mx || gy >= a.my) continue;
         double sum = 0.0;
         for (int c = 0; c < s_n; ++c) sum += a.scratch[s_off[c] + p];
@@ -1007,6 +1027,8 @@ cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, doub
     a.batch = batch;
     a.tiles_x = (a.mx + TX - 1) / TX;
     a.tiles_y = (a.my + L - 1) / L;
+    a.txt = TX;
+    a.tyt = L;
     a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1137,16 +1159,36 @@ bool build_canon<f2::ShapeStiffA>(const iga_lr_op* op, const Plan& pl, std::vect
     return !out->empty() && out->size() <= (size_t)f2::kMaxRounds2;
 }
 
-static int env_wpq() {
-    const char* s = getenv("IGALR_WPQ");
-    return (s && s[0] == '1') ? 1 : 2;
+template <int P>
+struct CanonCfg {
+    static constexpr int LW = P == 3 ? 16 : 12;  // rows per warp (TMEM: LW * ring cols <= 256)
+    static constexpr int WPQ = 2;                // warps per TMEM lane quadrant
+};
+
+// tile shape: QX quadrants across x; pick the least padding waste (ties -> wider)
+static int pick_qx(int mx, int my, int P) {
+    const int LW = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
+    int best = 4;
+    double bw = 1e30;
+    for (int qx : {4, 2, 1}) {
+        const int tx = 32 * qx, ty = LW * 2 * (4 / qx);
+        const double waste = (double)((mx + tx - 1) / tx * tx) / mx * (double)((my + ty - 1) / ty * ty) / my;
+        if (waste < bw - 1e-9) {
+            bw = waste;
+            best = qx;
+        }
+    }
+    const char* s = getenv("IGALR_QX");
+    if (s && (s[0] == '1' || s[0] == '2' || s[0] == '4')) best = s[0] - '0';
+    return best;
 }
 
-template <class S, int P, int LW, int WPQ>
+template <class S, int P, int QX, bool YRES>
 cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st) {
     using namespace f2;
-    constexpr int TY = LW * WPQ;
+    constexpr int LW = CanonCfg<P>::LW, WPQ = CanonCfg<P>::WPQ;
+    constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
     Args2 a;
     memset(&a, 0, sizeof a);
     a.src = src;
@@ -1162,8 +1204,10 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     a.my = op->m[1];
     a.mz = op->m[2];
     a.batch = batch;
-    a.tiles_x = (a.mx + TX - 1) / TX;
-    a.tiles_y = (a.my + TY - 1) / TY;
+    a.tiles_x = (a.mx + TXT - 1) / TXT;
+    a.tiles_y = (a.my + TYT - 1) / TYT;
+    a.txt = TXT;
+    a.tyt = TYT;
     a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1174,38 +1218,66 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     if (nct < 1) nct = 1;
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
     a.nctas = (int)nct;
-    const size_t sm = smem_bytes_canon<S, P, LW, WPQ>(a.nrounds);
-    auto kern = k_canon<S, P, LW, WPQ>;
+    const size_t sm = smem_bytes_canon<S, P, LW, WPQ, QX, YRES>(a.nrounds);
+    auto kern = k_canon<S, P, LW, WPQ, QX, YRES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
-    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TY * TX;
+    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
     e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
     if (e) return e;
     kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a);
     e = cudaGetLastError();
-    if (!e) {
-        if (a.nctas > 1) k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, TY);
+    if (!e && a.nctas > 1) {
+        k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, TYT);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
     return e;
 }
 
+template <class S, int P, int QX>
+bool yres_fits(int nrounds) {
+    return f2::smem_bytes_canon<S, P, CanonCfg<P>::LW, 2, QX, true>(nrounds) <= 227 * 1024;
+}
+
 template <class S>
-size_t canon_smem(int p, int wpq, int nrounds) {
-    if (p == 3) return wpq == 1 ? f2::smem_bytes_canon<S, 3, 32, 1>(nrounds) : f2::smem_bytes_canon<S, 3, 16, 2>(nrounds);
-    return wpq == 1 ? f2::smem_bytes_canon<S, 4, 24, 1>(nrounds) : f2::smem_bytes_canon<S, 4, 12, 2>(nrounds);
+size_t canon_smem(int p, int nrounds) {
+    // per-round y staging bounds the requirement of every tile shape
+    size_t m = 0;
+    if (p == 3) {
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 4, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 2, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 1, false>(nrounds));
+    } else {
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 4, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 2, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 1, false>(nrounds));
+    }
+    return m;
+}
+
+template <class S, int P, int QX>
+cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                           int accumulate, int batch, cudaStream_t st) {
+    const char* s = getenv("IGALR_YRES");
+    const bool force_off = s && s[0] == '0';
+    if (!force_off && yres_fits<S, P, QX>(pl.canon_nrounds))
+        return launch_canon_t<S, P, QX, true>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_t<S, P, QX, false>(op, pl, src, dst, scale, accumulate, batch, st);
 }
 
 template <class S>
 cudaError_t launch_canon(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                          int accumulate, int batch, cudaStream_t st) {
-    const int wpq = env_wpq();
-    if (op->p[0] == 3)
-        return wpq == 1 ? launch_canon_t<S, 3, 32, 1>(op, pl, src, dst, scale, accumulate, batch, st)
-                        : launch_canon_t<S, 3, 16, 2>(op, pl, src, dst, scale, accumulate, batch, st);
-    return wpq == 1 ? launch_canon_t<S, 4, 24, 1>(op, pl, src, dst, scale, accumulate, batch, st)
-                    : launch_canon_t<S, 4, 12, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+    const int qx = pick_qx(op->m[0], op->m[1], op->p[0]);
+    if (op->p[0] == 3) {
+        if (qx == 4) return launch_canon_q<S, 3, 4>(op, pl, src, dst, scale, accumulate, batch, st);
+        if (qx == 2) return launch_canon_q<S, 3, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+        return launch_canon_q<S, 3, 1>(op, pl, src, dst, scale, accumulate, batch, st);
+    }
+    if (qx == 4) return launch_canon_q<S, 4, 4>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (qx == 2) return launch_canon_q<S, 4, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_q<S, 4, 1>(op, pl, src, dst, scale, accumulate, batch, st);
 }
 
 template <class S>
@@ -1213,7 +1285,7 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
     std::vector<f2::RoundC<S>> v;
     if (!build_canon<S>(op, *pl, &v)) return IGA_EUNSUPPORTED;
     const int n = (int)v.size();
-    if (canon_smem<S>(op->p[0], 1, n) > 227 * 1024 || canon_smem<S>(op->p[0], 2, n) > 227 * 1024) return IGA_EUNSUPPORTED;
+    if (canon_smem<S>(op->p[0], n) > 227 * 1024) return IGA_EUNSUPPORTED;
     cudaError_t e = cudaMalloc(&pl->d_canon, sizeof(v[0]) * n);
     if (e) return cuda_error(e, "cudaMalloc(canon rounds)");
     e = cudaMemcpy(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice);
@@ -1248,8 +1320,11 @@ bool fused2_supported(const iga_lr_op* op) {
 
 bool fused2_preferred(const iga_lr_op* op, int batch) {
     // 128-wide tiles: narrow meshes waste lanes; small meshes cannot fill the persistent grid
+    // persistent CTAs need enough (tile, plane) units to fill the GPU
     const long long N = (long long)op->m[0] * op->m[1] * op->m[2] * batch;
-    return op->m[0] >= 96 && N >= (1LL << 21);
+    const char* s = getenv("IGALR_F2_MIN");
+    const long long thr = s ? atoll(s) : 0;
+    return N >= thr;
 }
 
 iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part) {

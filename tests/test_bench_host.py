@@ -1,0 +1,54 @@
+"""Host-side logic of bench.py on CPU: the multi-rank aggregation (world_size 2, gloo) and the
+reference arm's JSON contract (the oracle timed on the host cores)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(ws), RANK=str(rank),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import bench
+    import torch.distributed as dist
+    w, r, _ = bench.dist_setup("gloo")
+    # rank r pretends its timed region took (10 + r) ms over 5 steps on 1000 DoFs
+    val, ms = bench.weak_scaling_value(w, 1000, 10.0 + r, 5)
+    bench.barrier(w)
+    q.put((r, val, ms))
+    dist.destroy_process_group()
+
+
+def test_weak_scaling_aggregation_gloo_ws2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # both ranks agree: max time 11 ms over 5 steps -> 2.2 ms/step; 2 ranks x 1000 DoFs
+    for r, val, ms in res:
+        assert abs(ms - 2.2) < 1e-12
+        assert abs(val - 2 * 1000 / 2.2e-3 / 1e9) < 1e-15
+
+
+def test_reference_arm_json_contract():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--cpu-seconds", "0.6", "--config", "c2"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["impl"] == "reference" and d["unit"] == "GDoF/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
