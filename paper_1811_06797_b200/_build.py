@@ -17,7 +17,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
-SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_fused2.cu", "kkt.cu"]
+SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_fused2.cu", "canon_p3.cu",
+           "canon_p4.cu", "kkt.cu"]
 
 
 def _newer(src_paths, target):
@@ -32,6 +33,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INCLUDE, "iga_lr.h"))
     objs = []
+    jobs = []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
@@ -40,7 +42,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd = [NVCC] + ARCH + FLAGS + ["-I" + INCLUDE, "-I" + CSRC, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.check_call(cmd)
+            jobs.append(cmd)
+    # translation units compile in parallel (the canonical-kernel units dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for rc in ex.map(subprocess.call, jobs):
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, "nvcc")
     if force or _newer(objs, LIB):
         tmp = LIB + ".tmp.%d" % os.getpid()
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart=static"]

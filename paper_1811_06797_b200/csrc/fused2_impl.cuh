@@ -1,0 +1,1478 @@
+// apply_fused2.cu — fused sm_100a apply, version 2: TMEM-resident z-ring.
+//
+// One part (mass OR stiffness) per launch:
+//   y(z,y,x) = sum_rounds sum_g Fz_g *_z  sum_{j in g} c_j  Fy_j *_y  Fx_{e(j)} *_x  v
+// (Eqs. (massFinal)/(stiffnessFinal)).
+//
+// CTA = 4 warps (one per TMEM lane quadrant), tile = 128 x-columns x L y-rows of one batch
+// vector.  Persistent CTAs walk a contiguous range of (tile, z-plane) units; for every input
+// plane z' and plan round r each thread (one x-column) sweeps the L+2P rows of its column:
+//   X: t_e(y') = sum_k Fx_e[x][k] v(y', x-P+k)  (x-coefs in registers, v from the smem tile)
+//   Y: sliding register window over t_e; u_j = sum_k Fy_j[y][k] t_{e(j)}(y-P+k) (y-coefs are
+//      smem broadcasts), G_g = sum_j c_j u_j
+//   Z: ring(y,x)[slot] += Cz[g][slot] G_g  — the ring of 2P+1 output planes per point lives in
+//      TMEM (tcgen05.ld/st, 32x32b); slots are physical (plane mod 2P+1), the z-coefficients
+//      are permuted per z' instead of rotating the ring.
+// A plane is retired inline during the last round once its last input plane is processed.
+// Planes whose inputs span two CTAs' ranges are written to per-CTA scratch and summed by
+// k_fixup in CTA order (deterministic; no atomics).
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <type_traits>
+
+#include <cuda.h>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace igalr {
+namespace f2 {
+
+constexpr int TXW = 32;          // columns per warp
+constexpr int NW = 4;            // warps per CTA (one per TMEM lane quadrant)
+constexpr int TX = TXW * NW;     // 128 columns per tile
+constexpr int kMaxRounds2 = 40;
+
+template <int NX, int NP, int NG>
+struct Round2 {
+    int nx, np, ng, nyf;
+    int xf[NX];        // x factor of x-entry e
+    int yf[NP];        // distinct y factors of the round (nyf of them)
+    int pyf[NP];       // pair -> y-factor slot
+    int px[NP];        // pair -> x-entry
+    int pg[NP];        // pair -> group
+    int plead[NP];     // 1 if the pair is its group's lead (coef folded into the group scale)
+    double pc[NP];     // pair coefficient / group scale (unused for lead pairs)
+    int gf[NG];        // group z factor
+    double gs[NG];     // group scale (lead pair coefficient)
+};
+
+struct Args2 {
+    const double* src;
+    double* dst;
+    double scale;
+    int accumulate;
+    double* scratch;       // [nctas][NSEG][4P][L][TX] partial planes
+    const double* bx;
+    const double* by;
+    const double* bz;
+    const void* rounds;
+    int nrounds;
+    int mx, my, mz, batch;
+    int tiles_x, tiles_y;
+    long long units;       // tiles * mz
+    int nctas;
+    int txt, tyt;          // tile width / height (fixup)
+};
+
+constexpr int NSEG = 4;    // max segments per CTA (checked on the host)
+
+__host__ __device__ inline long long unit_begin(long long k, long long units, int nctas) {
+    return k * units / nctas;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+// ---- mbarrier / TMA helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- TMEM helpers (32x32b shape: each thread accesses its own lane)
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, double* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    // the wait "modifies" the destination registers so no use can be scheduled before it
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const double* v) {
+    uint32_t r[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        r[2 * k] = __double2loint(v[k]);
+        r[2 * k + 1] = __double2hiint(v[k]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, double* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]));
+    v[0] = __hiloint2double(r[1], r[0]);
+    v[1] = __hiloint2double(r[3], r[2]);
+}
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const double* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__double2loint(v[0])),
+                 "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])));
+}
+__device__ __forceinline__ double tm_ld1(uint32_t taddr) {
+    uint32_t lo, hi;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(lo), "+r"(hi));
+    return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__double2loint(v)),
+                 "r"(__double2hiint(v)));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ring slots per point, padded to a multiple of 8 doubles (x16 loads) or +2 (x4 tail)
+template <int BW>
+struct RingShape {
+    static constexpr int REM = BW % 8;
+    static constexpr int N16 = BW / 8 + (REM >= 5 ? 1 : 0);     // number of x16 chunks (8 doubles)
+    static constexpr int N4 = (REM >= 5 || REM == 0) ? 0 : (REM + 1) / 2;  // x4 chunks (2 doubles)
+    static constexpr int DBL = N16 * 8 + N4 * 2;  // doubles stored per point
+    static constexpr int COLS = DBL * 2;          // TMEM columns per point
+};
+
+template <int BW>
+__device__ __forceinline__ void ring_ld(uint32_t t, double* v) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) tm_ld16(t + c * 16, v + c * 8);
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) tm_ld4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+}
+template <int BW>
+__device__ __forceinline__ void ring_st(uint32_t t, const double* v) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) tm_st16(t + c * 16, v + c * 8);
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) tm_st4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+}
+
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// split TMEM ring load: issue now, wait (tied to the registers) when the values are needed
+template <int BW>
+__device__ __forceinline__ void ring_issue(uint32_t t, uint32_t* r) {
+    using RS = RingShape<BW>;
+#pragma unroll
+    for (int c = 0; c < RS::N16; ++c) {
+        uint32_t* q = r + c * 16;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+              "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+            : "r"(t + c * 16));
+    }
+#pragma unroll
+    for (int c = 0; c < RS::N4; ++c) {
+        uint32_t* q = r + RS::N16 * 16 + c * 4;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+                     : "r"(t + RS::N16 * 16 + c * 4));
+    }
+}
+template <int BW>
+__device__ __forceinline__ void ring_wait(uint32_t* r, double* v) {
+    using RS = RingShape<BW>;
+    static_assert(RS::DBL * 2 <= 24, "ring_wait handles up to 24 registers");
+    if constexpr (RS::DBL * 2 == 16) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                       "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                       "+r"(r[15]));
+    } else if constexpr (RS::DBL * 2 == 20) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                       "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                       "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]));
+    } else {
+#pragma unroll
+        for (int k = 0; k < RS::DBL * 2; ++k) asm volatile("" : "+r"(r[k]));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+#pragma unroll
+    for (int k = 0; k < RS::DBL; ++k) v[k] = __hiloint2double(r[2 * k + 1], r[2 * k]);
+}
+
+template <int P, int L>
+struct Geo {
+    static constexpr int BW = 2 * P + 1;
+    static constexpr int HY = L + 2 * P;          // sweep rows (incl. y-halo)
+    static constexpr int HX = TX + 2 * P;         // tile columns incl. x-halo
+    static constexpr int HXP = HX + 1;            // padded row pitch
+};
+
+// scratch slot of a partial output plane zo for a segment [za, zb) (see header comment)
+__device__ __forceinline__ int partial_slot(int zo, int za, int zb, int P) {
+    const int rel = zo - (za - P);
+    if (rel < 2 * P) return rel;                  // head band
+    return 2 * P + (zo - (zb - P));               // tail band
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+__global__ void __launch_bounds__(NW * 32, 1) k_fused2(const Args2 a) {
+    using G_ = Geo<P, L>;
+    constexpr int BW = G_::BW, HY = G_::HY, HXP = G_::HXP;
+    using RS = RingShape<BW>;
+    using RoundT = Round2<NX, NP, NG>;
+    static_assert(L * RS::COLS <= 512, "ring does not fit in TMEM");
+
+    extern __shared__ __align__(16) double sm[];
+    double* vin = sm;                                   // [2][HY][HXP]
+    double* xcs = vin + 2 * HY * HXP;                   // [2][NX][TX][BW]
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nrounds][NY][L][BW]  (by y-factor slot)
+    double* zcs = ycs + (size_t)a.nrounds * NY * L * BW;  // [2][nrounds][NG][BW]
+    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cx = warp * TXW + lane;  // tile column of this thread
+
+    // ---- TMEM allocation (512 columns, one CTA per SM)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < a.nrounds * (int)(sizeof(RoundT) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(rs)[i] = reinterpret_cast<const int*>(a.rounds)[i];
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(warp * 32) << 16);
+
+    const long long plane = (long long)a.mx * a.my;
+    const long long u0 = unit_begin(blockIdx.x, a.units, a.nctas);
+    const long long u1 = unit_begin(blockIdx.x + 1, a.units, a.nctas);
+
+    int seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / a.mz;
+        const int za = (int)(u - tile * a.mz);
+        const int zb = (int)min((long long)a.mz, (long long)za + (u1 - u));
+        u += zb - za;
+        long long tt = tile;
+        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+        const int b = (int)tt;
+        const int x0 = txi * TX, y0 = tyi * L;
+        const long long vb = (long long)b * a.mz * plane;
+        const int gx = x0 + cx;
+
+        // ---- stage y-coefficients of this tile (all rounds), clear the ring
+        __syncthreads();
+        for (int r = 0; r < a.nrounds; ++r) {
+            const RoundT& R = rs[r];
+            for (int i = threadIdx.x; i < R.nyf * L * BW; i += blockDim.x) {
+                const int s = i / (L * BW), rem = i - s * L * BW;
+                const int row = rem / BW, k = rem - row * BW;
+                const int gy = y0 + row;
+                const bool ok = gy < a.my;
+                cp8(ycs + ((size_t)(r * NY + s) * L + row) * BW + k,
+                    ok ? a.by + ((size_t)R.yf[s] * a.my + gy) * BW + k : a.by, ok);
+            }
+        }
+        {
+            double zero[RS::DBL];
+#pragma unroll
+            for (int k = 0; k < RS::DBL; ++k) zero[k] = 0.0;
+            for (int i = 0; i < L; ++i) ring_st<BW>(tbase + i * RS::COLS, zero);
+        }
+
+        auto stage_plane = [&](int zp, int buf) {
+            double* dstp = vin + buf * HY * HXP;
+            const double* srcp = a.src + vb + (long long)zp * plane;
+            for (int i = threadIdx.x; i < HY * G_::HX; i += blockDim.x) {
+                const int r = i / G_::HX, c = i - r * G_::HX;
+                const int gy = y0 - P + r, gxx = x0 - P + c;
+                const bool ok = gy >= 0 && gy < a.my && gxx >= 0 && gxx < a.mx;
+                cp8(dstp + r * HXP + c, ok ? srcp + (long long)gy * a.mx + gxx : a.src, ok);
+            }
+            // z-coefficients of plane zp for all rounds, permuted to physical ring slots:
+            // slot j holds output plane zo with zo == j (mod BW); coefficient Fz[zo][zp - zo + P]
+            double* zdst = zcs + buf * a.nrounds * NG * BW;
+            for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
+                const int r = i / (NG * BW), rem = i - r * NG * BW;
+                const int g = rem / BW, j = rem - g * BW;
+                const RoundT& R = rs[r];
+                int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;  // plane in [zp-P, zp+P] with zo%BW == j
+                const bool ok = g < R.ng && zo >= 0 && zo < a.mz;
+                cp8(zdst + i, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
+            }
+        };
+        auto stage_xc = [&](int r, int buf) {
+            const RoundT& R = rs[r];
+            double* dstp = xcs + buf * NX * TX * BW;
+            for (int i = threadIdx.x; i < R.nx * TX * BW; i += blockDim.x) {
+                const int e = i / (TX * BW), rem = i - e * TX * BW;
+                const int c = rem / BW, k = rem - c * BW;
+                const int g = x0 + c;
+                const bool ok = g < a.mx;
+                cp8(dstp + i, ok ? a.bx + ((size_t)R.xf[e] * a.mx + g) * BW + k : a.bx, ok);
+            }
+        };
+
+        const int zlo = za, zhi = zb;
+        stage_plane(zlo, 0);
+        stage_xc(0, 0);
+        cp_commit();
+        int pbuf = 0, xbuf = 0;
+        for (int zp = zlo; zp < zhi; ++zp) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                // prefetch: next round's x-coefs (and the next plane at the start of the plane)
+                const bool last_round = (r == a.nrounds - 1);
+                cp_wait<0>();
+                tm_wait_st();
+                __syncthreads();
+                if (!last_round) {
+                    stage_xc(r + 1, xbuf ^ 1);
+                } else if (zp + 1 < zhi) {
+                    stage_xc(0, xbuf ^ 1);
+                }
+                if (r == 0 && zp + 1 < zhi) stage_plane(zp + 1, pbuf ^ 1);
+                cp_commit();
+
+                const RoundT& R = rs[r];
+                const double* vt = vin + pbuf * HY * HXP;
+                const double* xc = xcs + xbuf * NX * TX * BW;
+                const double* yc = ycs + (size_t)r * NY * L * BW;
+                const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
+                double xr[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) xr[e][k] = (e < R.nx) ? xc[(e * TX + cx) * BW + k] : 0.0;
+                double zr[NG][BW];
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                    for (int j = 0; j < BW; ++j) zr[g][j] = (g < R.ng) ? zc[g * BW + j] * R.gs[g] : 0.0;
+                // retire slot of output plane zp - P in the last round (if complete here)
+                const int zret = zp - P;
+                const int jret = ((zret % BW) + BW) % BW;
+                bool ret_valid = false, ret_complete = false;
+                if (last_round && zret >= 0 && zret < a.mz) {
+                    ret_valid = true;
+                    const int lo = max(0, zret - P), hi = min(a.mz - 1, zret + P);
+                    ret_complete = lo >= za && hi <= zb - 1;
+                }
+
+                double w[NX][BW];  // circular window of t_e over the last BW rows
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) w[e][k] = 0.0;
+
+#pragma unroll 1
+                for (int base = 0; base < HY; base += BW) {
+#pragma unroll
+                    for (int q = 0; q < BW; ++q) {
+                        const int step = base + q;
+                        if (step < HY) {
+                            // X stage for sweep row `step`
+                            double v[BW];
+#pragma unroll
+                            for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + cx + k];
+#pragma unroll
+                            for (int e = 0; e < NX; ++e) {
+                                double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                                for (int k = 0; k < BW; k += 2) acc0 = fma(xr[e][k], v[k], acc0);
+#pragma unroll
+                                for (int k = 1; k < BW; k += 2) acc1 = fma(xr[e][k], v[k], acc1);
+                                w[e][q] = acc0 + acc1;
+                            }
+                            if (step >= 2 * P) {
+                                const int i = step - 2 * P;  // output row in tile
+                                const uint32_t tp = tbase + i * RS::COLS;
+                                double ring[RS::DBL];
+                                ring_ld<BW>(tp, ring);
+                                double G[NG];
+#pragma unroll
+                                for (int g = 0; g < NG; ++g) G[g] = 0.0;
+                                const double* ycr = yc + (size_t)i * BW;
+#pragma unroll
+                                for (int j = 0; j < NP; ++j) {
+                                    if (j < R.np) {
+                                        const double* fy = ycr + (size_t)R.pyf[j] * L * BW;
+                                        const int e = R.px[j];
+                                        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+                                        for (int ee = 0; ee < NX; ++ee) {
+                                            if (ee == e) {
+#pragma unroll
+                                                for (int k = 0; k < BW; k += 2) u0 = fma(fy[k], w[ee][(q + 1 + k) % BW], u0);
+#pragma unroll
+                                                for (int k = 1; k < BW; k += 2) u1 = fma(fy[k], w[ee][(q + 1 + k) % BW], u1);
+                                            }
+                                        }
+                                        const double u = u0 + u1;
+                                        const int g = R.pg[j];
+#pragma unroll
+                                        for (int gg = 0; gg < NG; ++gg)
+                                            if (gg == g) G[gg] = R.plead[j] ? G[gg] + u : fma(R.pc[j], u, G[gg]);
+                                    }
+                                }
+#pragma unroll
+                                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                                if (ret_valid) {
+                                    double val = 0.0;
+#pragma unroll
+                                    for (int j = 0; j < BW; ++j)
+                                        if (j == jret) {
+                                            val = ring[j];
+                                            ring[j] = 0.0;
+                                        }
+                                    const int gy = y0 + i;
+                                    if (gy < a.my && gx < a.mx) {
+                                        if (ret_complete) {
+                                            const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                            a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                        } else {
+                                            const int slot = partial_slot(zret, za, zb, P);
+                                            a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx] =
+                                                a.scale * val;
+                                        }
+                                    }
+                                }
+                                ring_st<BW>(tp, ring);
+                            }
+                        }
+                    }
+                }
+                if (last_round) pbuf ^= 1;
+                xbuf ^= 1;
+            }
+        }
+        // ---- flush planes still in the ring: zo in [zb-P, zb+P) (partial unless zb == mz)
+        tm_wait_st();
+        __syncthreads();
+        for (int i = 0; i < L; ++i) {
+            const uint32_t tp = tbase + i * RS::COLS;
+            double ring[RS::DBL];
+            ring_ld<BW>(tp, ring);
+            const int gy = y0 + i;
+#pragma unroll
+            for (int s = 0; s < 2 * P; ++s) {
+                const int zo = zb - P + s;
+                if (zo < 0 || zo >= a.mz || zo < za - P) continue;
+                // already retired inline? planes zo <= zb-1-P were retired during the sweep
+                if (zo <= zb - 1 - P) continue;
+                const int j = zo % BW;
+                double val = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BW; ++jj)
+                    if (jj == j) val = ring[jj];
+                if (gy < a.my && gx < a.mx) {
+                    const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+                    const bool complete = lo >= za && hi <= zb - 1;
+                    if (complete) {
+                        const long long o = vb + (long long)zo * plane + (long long)gy * a.mx + gx;
+                        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                    } else {
+                        const int slot = partial_slot(zo, za, zb, P);
+                        a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * L + i) * TX + cx] = a.scale * val;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
+}
+
+// ------------------------------------------------------------------------------------
+// Canonical round shapes: the plan structure is compile-time, only factor ids and the
+// pair/group coefficients are runtime data.  Stiffness (reading A of G6): for
+// every r the 9 blocks q_kl share v_r, giving x-entries [K,E,T,M] (patterns (1,1),(0,1),
+// (1,0),(0,0)), y-factors [M,T,E,K], z-groups [M,T,E,K] and the 9 (y,x)->z pairs below.
+struct ShapeStiffA {
+    static constexpr int NX = 4, NY = 4, NG = 4, NPAIR = 9;
+    __host__ __device__ static constexpr int px(int j) { return j == 0 ? 0 : (j <= 2 ? 1 : (j == 3 || j == 6) ? 2 : 3); }
+    __host__ __device__ static constexpr int py(int j) {
+        return (j == 0 || j == 2 || j == 6 || j == 8) ? 0 : (j == 1 || j == 7) ? 1 : (j == 3 || j == 5) ? 2 : 3;
+    }
+    __host__ __device__ static constexpr int pg(int j) {
+        return (j == 0 || j == 1 || j == 3 || j == 4) ? 0 : (j == 2 || j == 5) ? 1 : (j == 6 || j == 7) ? 2 : 3;
+    }
+    __host__ __device__ static constexpr bool lead(int j) { return j == 0 || j == 2 || j == 6 || j == 8; }
+};
+// Mass: K consecutive rank-one terms per sweep (independent pipelines sharing the input
+// loads and the ring).
+template <int K>
+struct ShapeMassK {
+    static constexpr int NX = K, NY = K, NG = K, NPAIR = K;
+    __host__ __device__ static constexpr int px(int j) { return j; }
+    __host__ __device__ static constexpr int py(int j) { return j; }
+    __host__ __device__ static constexpr int pg(int j) { return j; }
+    __host__ __device__ static constexpr bool lead(int) { return true; }
+};
+using ShapeMass = ShapeMassK<4>;
+
+template <class S>
+struct RoundC {
+    int xf[S::NX], yf[S::NY], gf[S::NG];
+    int pad;
+    double pc[S::NPAIR];   // coefficient ratio of non-lead pairs
+    double gs[S::NG];      // group scale (lead pair coefficient)
+};
+
+template <int P, int TXT_, int TY>
+struct GeoC {
+    static constexpr int BW = 2 * P + 1;
+    static constexpr int BWP = (BW + 1) & ~1;     // y-coef row pitch (16-byte aligned rows)
+    static constexpr int HY = TY + 2 * P;
+    static constexpr int HX = TXT_ + 2 * P;
+    static constexpr int HXP = HX + 1;
+};
+
+// QX of the 4 TMEM lane quadrants tile x (32 columns each); the other 4/QX stack in y.
+template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA>
+__global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int TX = 32 * QX;                 // tile columns (shadows the 128-wide default)
+    constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
+    using G_ = GeoC<P, TX, TY>;
+    constexpr int BW = G_::BW, BWP = G_::BWP, HY = G_::HY;
+    constexpr int HXP = G_::HXP;
+    constexpr int VSZ = (HY * G_::HXP + 15) & ~15;  // doubles per plane buffer (128-B aligned)
+    constexpr int NX = S::NX, NY = S::NY, NG = S::NG, NPAIR = S::NPAIR;
+    using RS = RingShape<BW>;
+    using RoundT = RoundC<S>;
+    static_assert(LW * RS::COLS * WPQ <= 512, "ring does not fit in TMEM");
+
+    extern __shared__ __align__(1024) double sm[];
+    double* vin = sm;                                   // [2][VSZ]  (HY x HXP planes)
+    double* xcs = vin + 2 * VSZ;                        // [2][NX][TX][BW]  (per round)
+    // y-coefficients: all rounds resident per segment (YRES) or double-buffered per round
+    constexpr int YSLOTS = YRES ? 0 : 2;
+    const int nyslots = YRES ? a.nrounds : YSLOTS;
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nyslots][NY][TY][BWP]
+    double* zcs = ycs + (size_t)nyslots * NY * TY * BWP;  // [2][nrounds][NG][BW] (per plane)
+    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ __align__(8) uint64_t xbar[2];  // bulk-copy completion of the x-coefficient buffers
+    uint32_t xph[2] = {0, 0};
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int quad = warp & 3, sub = warp >> 2;
+    const int cx = (quad % QX) * TXW + lane;                 // tile column of this thread
+    const int row0 = ((quad / QX) * WPQ + sub) * LW;          // first tile output row of this warp
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < a.nrounds * (int)(sizeof(RoundT) / 4); i += blockDim.x)
+        reinterpret_cast<int*>(rs)[i] = reinterpret_cast<const int*>(a.rounds)[i];
+    if (TMA && threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k) mbar_init(&xbar[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base_sh + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sub * (512 / WPQ));
+
+    const long long plane = (long long)a.mx * a.my;
+    const long long u0 = unit_begin(blockIdx.x, a.units, a.nctas);
+    const long long u1 = unit_begin(blockIdx.x + 1, a.units, a.nctas);
+
+    int seg = 0;
+    for (long long u = u0; u < u1; ++seg) {
+        const long long tile = u / a.mz;
+        const int za = (int)(u - tile * a.mz);
+        const int zb = (int)min((long long)a.mz, (long long)za + (u1 - u));
+        u += zb - za;
+        long long tt = tile;
+        const int txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+        const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+        const int b = (int)tt;
+        const int x0 = txi * TX, y0 = tyi * TY;
+        const long long vb = (long long)b * a.mz * plane;
+        const int gx = x0 + cx;
+
+        __syncthreads();
+        if constexpr (YRES) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                const RoundT& R = rs[r];
+                double* ydst = ycs + (size_t)r * NY * TY * BWP;
+                if (lane < BW) {
+                    for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
+                        const int f = rr / TY, row = rr - f * TY;
+                        cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
+                    }
+                }
+            }
+        }
+        {
+            double zero[RS::DBL];
+#pragma unroll
+            for (int k = 0; k < RS::DBL; ++k) zero[k] = 0.0;
+            for (int i = 0; i < LW; ++i) ring_st<BW>(tbase + i * RS::COLS, zero);
+        }
+
+        auto stage_plane = [&](int zp, int buf) {
+            double* dstp = vin + buf * VSZ;
+            const double* srcp = a.src + vb + (long long)zp * plane;
+            {
+                // (tensor-map boxes would give free OOB zero fill, but starting a box at a
+                // negative coordinate faults on this stack — tools/tma_test.cu — so the halo'd
+                // plane tile is staged with 8-byte cp.async)
+                // rows by warp, contiguous columns by lane: no per-element division
+                for (int r = warp; r < HY; r += NW * WPQ) {
+                    const int gy = y0 - P + r;
+                    const bool rowok = gy >= 0 && gy < a.my;
+                    const double* srow = srcp + (long long)gy * a.mx + (x0 - P);
+                    for (int c = lane; c < G_::HX; c += 32) {
+                        const int gxx = x0 - P + c;
+                        const bool ok = rowok && gxx >= 0 && gxx < a.mx;
+                        cp8(dstp + r * HXP + c, ok ? srow + c : a.src, ok);
+                    }
+                }
+            }
+            double* zdst = zcs + buf * a.nrounds * NG * BW;
+            for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
+                const int r = i / (NG * BW), rem = i - r * NG * BW;
+                const int g = rem / BW, j = rem - g * BW;
+                const RoundT& R = rs[r];
+                const int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;
+                const bool ok = zo >= 0 && zo < a.mz;
+                cp8(zdst + i, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
+            }
+        };
+        auto stage_xc = [&](int r, int buf) {
+            // each factor's band rows for the tile's columns (rows) are one contiguous block
+            // (entries past mx / my read the band allocation's padding or the next factor and
+            // are never used for an output)
+            const RoundT& R = rs[r];
+            double* dstp = xcs + buf * NX * TX * BW;
+            if constexpr (TMA) {
+                if (threadIdx.x == 0) {
+                    mbar_expect_tx(&xbar[buf], (uint32_t)(NX * TX * BW * sizeof(double)));
+#pragma unroll
+                    for (int e = 0; e < NX; ++e)
+                        bulk_g2s(dstp + e * TX * BW, a.bx + ((size_t)R.xf[e] * a.mx + x0) * BW,
+                                 (uint32_t)(TX * BW * sizeof(double)), &xbar[buf]);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < NX; ++e) {
+                    const double* src = a.bx + ((size_t)R.xf[e] * a.mx + x0) * BW;
+                    for (int i = threadIdx.x; i < TX * BW; i += blockDim.x) cp8(dstp + e * TX * BW + i, src + i, true);
+                }
+            }
+            // y rows re-pitched from BW to BWP (16-byte aligned) for LDS.128 broadcasts
+            if (YRES) return;
+            double* ydst = ycs + buf * NY * TY * BWP;
+            if (lane < BW) {
+                for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
+                    const int f = rr / TY, row = rr - f * TY;
+                    cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
+                }
+            }
+        };
+
+        stage_plane(za, 0);
+        stage_xc(0, 0);
+        cp_commit();
+        int pbuf = 0, xbuf = 0;
+        for (int zp = za; zp < zb; ++zp) {
+            for (int r = 0; r < a.nrounds; ++r) {
+                const bool last_round = (r == a.nrounds - 1);
+                if constexpr (TMA) {  // x-coefficients arrive by cp.async.bulk (mbarrier)
+                    mbar_wait(&xbar[xbuf], xph[xbuf]);
+                    xph[xbuf] ^= 1;
+                }
+                cp_wait<0>();
+                tm_wait_st();
+                __syncthreads();
+                if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                if (r == 0 && zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
+                cp_commit();
+
+                const RoundT& R = rs[r];
+                const double* vt = vin + pbuf * VSZ + row0 * HXP + cx;
+                const double* xc = xcs + xbuf * NX * TX * BW;
+                const double* yc = ycs + (size_t)(YRES ? r : xbuf) * NY * TY * BWP + (size_t)row0 * BWP;
+                const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
+                double xr[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) xr[e][k] = xc[(e * TX + cx) * BW + k];
+                double zr[NG][BW];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    const double gsc = R.gs[g];
+#pragma unroll
+                    for (int j = 0; j < BW; ++j) zr[g][j] = zc[g * BW + j] * gsc;
+                }
+                double pc[NPAIR];
+#pragma unroll
+                for (int j = 0; j < NPAIR; ++j) pc[j] = R.pc[j];
+                const int zret = zp - P;
+                const int jret = ((zret % BW) + BW) % BW;
+                bool ret_valid = false, ret_complete = false;
+                if (last_round && zret >= 0 && zret < a.mz) {
+                    ret_valid = true;
+                    const int lo = max(0, zret - P), hi = min(a.mz - 1, zret + P);
+                    ret_complete = lo >= za && hi <= zb - 1;
+                }
+
+                double w[NX][BW];
+#pragma unroll
+                for (int e = 0; e < NX; ++e)
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) w[e][k] = 0.0;
+
+                // X stage of sweep row `step` into window slot Q (compile-time)
+                auto xstage = [&](auto Qc, int step) {
+                    constexpr int Q = decltype(Qc)::value;
+                    double v[BW];
+#pragma unroll
+                    for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
+#pragma unroll
+                    for (int e = 0; e < NX; ++e) {
+                        double acc = xr[e][0] * v[0];
+#pragma unroll
+                        for (int k = 1; k < BW; ++k) acc = fma(xr[e][k], v[k], acc);
+                        w[e][Q] = acc;
+                    }
+                };
+                // Y + Z stages for output row i (window newest row in slot Q)
+                auto yzstage = [&](auto Qc, int i) {
+                    constexpr int Q = decltype(Qc)::value;
+                    const uint32_t tp = tbase + i * RS::COLS;
+                    uint32_t rr[RS::DBL * 2];
+                    ring_issue<BW>(tp, rr);  // TMEM load in flight during the Y stage
+                    double G[NG];
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) G[g] = 0.0;
+                    const double* ycr = yc + (size_t)i * BWP;
+#pragma unroll
+                    for (int f = 0; f < NY; ++f) {
+                        double yv[BWP];
+                        const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
+#pragma unroll
+                        for (int k = 0; k < BWP / 2; ++k) {  // broadcast LDS.128
+                            const double2 t2 = y2[k];
+                            yv[2 * k] = t2.x;
+                            yv[2 * k + 1] = t2.y;
+                        }
+#pragma unroll
+                        for (int j = 0; j < NPAIR; ++j) {
+                            if (S::py(j) != f) continue;
+                            const int e = S::px(j);
+                            const int g = S::pg(j);
+                            if (S::lead(j)) {
+                                // lead pair: accumulate straight into its group value
+#pragma unroll
+                                for (int k = 0; k < BW; ++k) G[g] = fma(yv[k], w[e][(Q + 1 + k) % BW], G[g]);
+                            } else {
+                                double u = yv[0] * w[e][(Q + 1) % BW];
+#pragma unroll
+                                for (int k = 1; k < BW; ++k) u = fma(yv[k], w[e][(Q + 1 + k) % BW], u);
+                                G[g] = fma(pc[j], u, G[g]);
+                            }
+                        }
+                    }
+                    double ring[RS::DBL];
+                    ring_wait<BW>(rr, ring);
+#pragma unroll
+                    for (int g = 0; g < NG; ++g)
+#pragma unroll
+                        for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                    ring_st<BW>(tp, ring);
+                };
+                constexpr int HYW = LW + 2 * P;        // rows swept by this warp
+                constexpr int NFULL = (HYW - BW) / BW;  // full blocks after block 0
+                constexpr int REM = (HYW - BW) % BW;
+                // block 0: the first 2P rows only fill the window
+                static_for<0, BW>([&](auto Qc) {
+                    constexpr int Q = decltype(Qc)::value;
+                    xstage(Qc, Q);
+                    if constexpr (Q >= 2 * P) yzstage(Qc, Q - 2 * P);
+                });
+#pragma unroll 1
+                for (int blk = 1; blk <= NFULL; ++blk) {
+                    static_for<0, BW>([&](auto Qc) {
+                        const int step = blk * BW + decltype(Qc)::value;
+                        xstage(Qc, step);
+                        yzstage(Qc, step - 2 * P);
+                    });
+                }
+                static_for<0, REM>([&](auto Qc) {
+                    const int step = (NFULL + 1) * BW + decltype(Qc)::value;
+                    xstage(Qc, step);
+                    yzstage(Qc, step - 2 * P);
+                });
+                if (ret_valid) {
+                    // plane zret is final: write it (or its partial) out and clear its slot
+                    tm_wait_st();
+                    for (int i = 0; i < LW; ++i) {
+                        const uint32_t ts = tbase + i * RS::COLS + 2 * jret;
+                        const double val = tm_ld1(ts);
+                        tm_st1(ts, 0.0);
+                        const int gy = y0 + row0 + i;
+                        if (gy < a.my && gx < a.mx) {
+                            if (ret_complete) {
+                                const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                            } else {
+                                const int slot = partial_slot(zret, za, zb, P);
+                                a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                                    a.scale * val;
+                            }
+                        }
+                    }
+                }
+                if (last_round) pbuf ^= 1;
+                xbuf ^= 1;
+            }
+        }
+        tm_wait_st();
+        __syncthreads();
+        for (int i = 0; i < LW; ++i) {
+            const uint32_t tp = tbase + i * RS::COLS;
+            double ring[RS::DBL];
+            ring_ld<BW>(tp, ring);
+            const int gy = y0 + row0 + i;
+#pragma unroll
+            for (int s = 0; s < 2 * P; ++s) {
+                const int zo = zb - P + s;
+                if (zo < 0 || zo >= a.mz) continue;
+                const int j = zo % BW;
+                double val = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BW; ++jj)
+                    if (jj == j) val = ring[jj];
+                if (gy < a.my && gx < a.mx) {
+                    const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+                    const bool complete = lo >= za && hi <= zb - 1;
+                    if (complete) {
+                        const long long o = vb + (long long)zo * plane + (long long)gy * a.mx + gx;
+                        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                    } else {
+                        const int slot = partial_slot(zo, za, zb, P);
+                        a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                            a.scale * val;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh));
+}
+
+template <class S, int P, int LW, int WPQ, int QX, bool YRES>
+size_t smem_bytes_canon(int nrounds) {
+    constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
+    using G_ = GeoC<P, TXT, TYT>;  // (padded pitch; the TMA variant uses the dense pitch, <= this)
+    const size_t ys = YRES ? (size_t)nrounds : 2;
+    const size_t vsz = (G_::HY * G_::HXP + 15) & ~(size_t)15;
+    return sizeof(double) * (2 * vsz + 2 * S::NX * TXT * G_::BW + ys * S::NY * TYT * G_::BWP +
+                             2 * (size_t)nrounds * S::NG * G_::BW) +
+           sizeof(RoundC<S>) * nrounds + 64;
+}
+
+// Sum partial planes.  Only planes within P of a CTA-range boundary inside a tile can have
+// inputs in several CTA ranges; one CTA per (boundary, plane offset) finds the contributing
+// CTA segments once (thread 0) and all threads add their scratch entries in increasing CTA
+// order (deterministic).
+static __global__ void k_fixup(const Args2 a, int P, int L) {
+    __shared__ int s_valid, s_n, s_b, s_zo, s_txi, s_tyi;
+    __shared__ long long s_off[8];
+    const int kb = 1 + blockIdx.x / (2 * P);
+    const int s = blockIdx.x % (2 * P);
+    if (threadIdx.x == 0) {
+        s_valid = 0;
+        s_n = 0;
+        const long long ub = unit_begin(kb, a.units, a.nctas);
+        const long long tile = ub / a.mz;
+        const int zbnd = (int)(ub - tile * a.mz);
+        const int zo = zbnd - P + s;
+        if (zbnd != 0 && zo >= 0 && zo < a.mz) {
+            long long tt = tile;
+            s_txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+            s_tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+            s_b = (int)tt;
+            s_zo = zo;
+            const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+            const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
+            long long k0 = kb - 1, k1 = kb;
+            while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
+            while (k1 + 1 < a.nctas && unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
+            for (long long k = k0; k <= k1 && s_n < 8; ++k) {
+                const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
+                int seg = 0;
+                for (long long u = cu0; u < cu1; ++seg) {
+                    const long long t2 = u / a.mz;
+                    const int sa = (int)(u - t2 * a.mz);
+                    const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
+                    if (t2 == tile) {
+                        const int slot = partial_slot(zo, sa, sb, P);
+                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)a.tyt * a.txt;
+                        break;
+                    }
+                    u += sb - sa;
+                }
+            }
+            s_valid = 1;
+        }
+    }
+    __syncthreads();
+    if (!s_valid) return;
+    const long long plane = (long long)a.mx * a.my;
+    const long long obase = (long long)s_b * a.mz * plane + (long long)s_zo * plane;
+    for (int p = threadIdx.x; p < a.tyt * a.txt; p += blockDim.x) {
+        const int i = p / a.txt, cx = p - i * a.txt;
+        const int gx = s_txi * a.txt + cx, gy = s_tyi * a.tyt + i;
+        if (gx >= a.mx || gy >= a.my) continue;
+        double sum = 0.0;
+        for (int c = 0; c < s_n; ++c) sum += a.scratch[s_off[c] + p];
+        const long long o = obase + (long long)gy * a.mx + gx;
+        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + sum;
+    }
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+size_t smem_bytes(int nrounds) {
+    using G_ = Geo<P, L>;
+    constexpr int BW = G_::BW;
+    return sizeof(double) * (2 * G_::HY * G_::HXP + 2 * NX * TX * BW + (size_t)nrounds * NY * L * BW +
+                             2 * (size_t)nrounds * NG * BW) +
+           sizeof(Round2<NX, NP, NG>) * nrounds + 64;
+}
+
+}  // namespace f2
+
+// ---------------------------------------------------------------------------------- host
+namespace {
+
+template <int NX, int NP, int NG, int NY>
+bool build_rounds2(const Plan& pl, std::vector<f2::Round2<NX, NP, NG>>* out) {
+    out->clear();
+    for (const Round& R : pl.rounds) {
+        // split pairs that feed several groups into one pair per group
+        f2::Round2<NX, NP, NG> F;
+        memset(&F, 0, sizeof F);
+        if (R.nx > NX || R.ng > NG) return false;
+        F.nx = R.nx;
+        F.ng = R.ng;
+        for (int e = 0; e < R.nx; ++e) F.xf[e] = R.xf[e];
+        for (int g = 0; g < R.ng; ++g) F.gf[g] = R.gf[g];
+        int np = 0;
+        bool lead_done[kMaxG] = {false, false, false, false, false};
+        for (int g = 0; g < R.ng; ++g) {
+            for (int e = 0; e < R.ne[g]; ++e) {
+                if (np >= NP) return false;
+                const int j = R.ep[g][e];
+                const int yfac = R.pf[j];
+                int s = -1;
+                for (int t = 0; t < F.nyf; ++t)
+                    if (F.yf[t] == yfac) s = t;
+                if (s < 0) {
+                    if (F.nyf >= NY) return false;
+                    s = F.nyf++;
+                    F.yf[s] = yfac;
+                }
+                F.pyf[np] = s;
+                F.px[np] = R.px[j];
+                F.pg[np] = g;
+                const double c = R.ec[g][e];
+                if (!lead_done[g] && c != 0.0) {
+                    F.plead[np] = 1;
+                    F.pc[np] = 1.0;
+                    F.gs[g] = c;
+                    lead_done[g] = true;
+                } else {
+                    F.plead[np] = 0;
+                    F.pc[np] = lead_done[g] ? c / F.gs[g] : 0.0;
+                }
+                ++np;
+            }
+            if (!lead_done[g]) F.gs[g] = 0.0;
+        }
+        F.np = np;
+        out->push_back(F);
+    }
+    return !out->empty() && (int)out->size() <= f2::kMaxRounds2;
+}
+
+// shape of the fused-v2 round tables per part
+constexpr int kSX = 4, kSP = 9, kSG = 4, kSY = 4;  // stiffness part
+constexpr int kMX = 1, kMP = 1, kMG = 1, kMY = 1;  // mass part
+
+template <int P>
+constexpr int rows_per_thread() {
+    return P == 3 ? 32 : (P == 4 ? 24 : (P == 2 ? 32 : 16));
+}
+
+template <int P, int L, int NX, int NP, int NG, int NY>
+cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale, int accumulate,
+                    int batch, cudaStream_t st) {
+    using namespace f2;
+    Args2 a;
+    memset(&a, 0, sizeof a);
+    a.src = src;
+    a.dst = dst;
+    a.scale = scale;
+    a.accumulate = accumulate;
+    a.bx = op->F[0].band;
+    a.by = op->F[1].band;
+    a.bz = op->F[2].band;
+    a.rounds = pl.d_f2;
+    a.nrounds = (int)pl.f2_nrounds;
+    a.mx = op->m[0];
+    a.my = op->m[1];
+    a.mz = op->m[2];
+    a.batch = batch;
+    a.tiles_x = (a.mx + TX - 1) / TX;
+    a.tiles_y = (a.my + L - 1) / L;
+    a.txt = TX;
+    a.tyt = L;
+    a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // persistent CTAs (one per SM); keep segments >= 2P+2 planes and <= 3 mz units per CTA
+    long long nct = sms;
+    const long long minlen = 2 * P + 2;
+    if (a.units / nct < minlen) nct = a.units / minlen;
+    if (nct < 1) nct = 1;
+    while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
+    a.nctas = (int)nct;
+    const size_t sm = smem_bytes<P, L, NX, NP, NG, NY>(a.nrounds);
+    auto kern = k_fused2<P, L, NX, NP, NG, NY>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * L * TX;
+    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    if (e) return e;
+    kern<<<a.nctas, NW * 32, sm, st>>>(a);
+    e = cudaGetLastError();
+    if (!e) {
+        if (a.nctas > 1) k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, L);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(a.scratch, st);
+    return e;
+}
+
+template <int P>
+cudaError_t launch_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                        int accumulate, int batch, cudaStream_t st) {
+    constexpr int L = rows_per_thread<P>();
+    if (part == 0) return launch2<P, L, kMX, kMP, kMG, kMY>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch2<P, L, kSX, kSP, kSG, kSY>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+
+
+// ---- canonical-shape host side
+template <class S>
+bool build_canon(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<S>>* out);
+
+template <>
+bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMass>>* out) {
+    (void)op;
+    constexpr int K = f2::ShapeMass::NX;
+    out->clear();
+    std::vector<const Round*> terms;
+    for (const Round& R : pl.rounds) {
+        if (R.nx != 1 || R.np != 1 || R.ng != 1 || R.ne[0] != 1) return false;
+        terms.push_back(&R);
+    }
+    if (terms.empty()) return false;
+    for (size_t i = 0; i < terms.size(); i += K) {
+        f2::RoundC<f2::ShapeMass> C;
+        memset(&C, 0, sizeof C);
+        for (int k = 0; k < K; ++k) {
+            const bool real = i + k < terms.size();
+            const Round& R = *terms[real ? i + k : 0];
+            C.xf[k] = R.xf[0];
+            C.yf[k] = R.pf[0];
+            C.gf[k] = R.gf[0];
+            C.gs[k] = real ? R.ec[0][0] : 0.0;  // padding term contributes exactly zero
+            C.pc[k] = 1.0;
+        }
+        out->push_back(C);
+    }
+    return out->size() <= (size_t)f2::kMaxRounds2;
+}
+
+template <>
+bool build_canon<f2::ShapeStiffA>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeStiffA>>* out) {
+    using S = f2::ShapeStiffA;
+    out->clear();
+    // pattern (a*2+b) -> canonical slot; x: [K,E,T,M], y and z: [M,T,E,K]
+    auto xslot = [](int pat) { return pat == 3 ? 0 : pat == 1 ? 1 : pat == 2 ? 2 : 3; };
+    auto yslot = [](int pat) { return pat == 0 ? 0 : pat == 2 ? 1 : pat == 1 ? 2 : 3; };
+    for (const Round& R : pl.rounds) {
+        f2::RoundC<S> C;
+        memset(&C, 0, sizeof C);
+        int xs[4] = {-1, -1, -1, -1}, ys[4] = {-1, -1, -1, -1}, gsl[4] = {-1, -1, -1, -1};
+        for (int e = 0; e < R.nx; ++e) {
+            const int s = xslot(op->F[0].pattern[R.xf[e]]);
+            if (xs[s] >= 0) return false;
+            xs[s] = R.xf[e];
+        }
+        for (int g = 0; g < R.ng; ++g) {
+            const int s = yslot(op->F[2].pattern[R.gf[g]]);
+            if (gsl[s] >= 0) return false;
+            gsl[s] = R.gf[g];
+        }
+        double cj[S::NPAIR];
+        bool seen[S::NPAIR] = {};
+        for (int g = 0; g < R.ng; ++g) {
+            const int gs_ = yslot(op->F[2].pattern[R.gf[g]]);
+            for (int e = 0; e < R.ne[g]; ++e) {
+                const int j = R.ep[g][e];
+                const int xsl = xslot(op->F[0].pattern[R.xf[R.px[j]]]);
+                const int ysl = yslot(op->F[1].pattern[R.pf[j]]);
+                if (ys[ysl] >= 0 && ys[ysl] != R.pf[j]) return false;
+                ys[ysl] = R.pf[j];
+                int cj_idx = -1;
+                for (int k = 0; k < S::NPAIR; ++k)
+                    if (S::px(k) == xsl && S::py(k) == ysl && S::pg(k) == gs_) cj_idx = k;
+                if (cj_idx < 0 || seen[cj_idx]) return false;
+                seen[cj_idx] = true;
+                cj[cj_idx] = R.ec[g][e];
+            }
+        }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (!seen[k]) return false;
+        for (int s = 0; s < 4; ++s)
+            if (xs[s] < 0 || ys[s] < 0 || gsl[s] < 0) return false;
+        for (int s = 0; s < 4; ++s) {
+            C.xf[s] = xs[s];
+            C.yf[s] = ys[s];
+            C.gf[s] = gsl[s];
+        }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (S::lead(k)) {
+                if (cj[k] == 0.0) return false;
+                C.gs[S::pg(k)] = cj[k];
+                C.pc[k] = 1.0;
+            }
+        for (int k = 0; k < S::NPAIR; ++k)
+            if (!S::lead(k)) C.pc[k] = cj[k] / C.gs[S::pg(k)];
+        out->push_back(C);
+    }
+    return !out->empty() && out->size() <= (size_t)f2::kMaxRounds2;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static EncodeFn tensor_map_encode() {
+    static EncodeFn fn = []() -> EncodeFn {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    return fn;
+}
+
+template <int P>
+struct CanonCfg {
+    static constexpr int LW = P == 3 ? 16 : 12;  // rows per warp (TMEM: LW * ring cols <= 256)
+    static constexpr int WPQ = 2;                // warps per TMEM lane quadrant
+};
+
+// tile shape: QX quadrants across x; pick the least padding waste (ties -> wider)
+static int pick_qx(int mx, int my, int P) {
+    const int LW = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
+    int best = 4;
+    double bw = 1e30;
+    for (int qx : {4, 2, 1}) {
+        const int tx = 32 * qx, ty = LW * 2 * (4 / qx);
+        const double waste = (double)((mx + tx - 1) / tx * tx) / mx * (double)((my + ty - 1) / ty * ty) / my;
+        if (waste < bw - 1e-9) {
+            bw = waste;
+            best = qx;
+        }
+    }
+    const char* s = getenv("IGALR_QX");
+    if (s && (s[0] == '1' || s[0] == '2' || s[0] == '4')) best = s[0] - '0';
+    return best;
+}
+
+template <class S, int P, int QX, bool YRES, bool TMA>
+cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                           int accumulate, int batch, cudaStream_t st) {
+    using namespace f2;
+    constexpr int LW = CanonCfg<P>::LW, WPQ = CanonCfg<P>::WPQ;
+    constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
+    Args2 a;
+    memset(&a, 0, sizeof a);
+    a.src = src;
+    a.dst = dst;
+    a.scale = scale;
+    a.accumulate = accumulate;
+    a.bx = op->F[0].band;
+    a.by = op->F[1].band;
+    a.bz = op->F[2].band;
+    a.rounds = pl.d_canon;
+    a.nrounds = pl.canon_nrounds;
+    a.mx = op->m[0];
+    a.my = op->m[1];
+    a.mz = op->m[2];
+    a.batch = batch;
+    a.tiles_x = (a.mx + TXT - 1) / TXT;
+    a.tiles_y = (a.my + TYT - 1) / TYT;
+    a.txt = TXT;
+    a.tyt = TYT;
+    a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long nct = sms;
+    const long long minlen = 2 * P + 2;
+    if (a.units / nct < minlen) nct = a.units / minlen;
+    if (nct < 1) nct = 1;
+    while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
+    a.nctas = (int)nct;
+    const size_t sm = smem_bytes_canon<S, P, LW, WPQ, QX, YRES>(a.nrounds);
+    auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA>;
+    CUtensorMap tmap;  // unused (kept in the signature for a future TMA plane path)
+    memset(&tmap, 0, sizeof tmap);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
+    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    if (e) return e;
+    kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a, tmap);
+    e = cudaGetLastError();
+    if (!e && a.nctas > 1) {
+        k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, TYT);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(a.scratch, st);
+    return e;
+}
+
+template <class S, int P, int QX>
+bool yres_fits(int nrounds) {
+    return f2::smem_bytes_canon<S, P, CanonCfg<P>::LW, 2, QX, true>(nrounds) <= 227 * 1024;
+}
+
+template <class S>
+size_t canon_smem(int p, int nrounds) {
+    // per-round y staging bounds the requirement of every tile shape
+    size_t m = 0;
+    if (p == 3) {
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 4, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 2, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 3, CanonCfg<3>::LW, 2, 1, false>(nrounds));
+    } else {
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 4, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 2, false>(nrounds));
+        m = std::max(m, f2::smem_bytes_canon<S, 4, CanonCfg<4>::LW, 2, 1, false>(nrounds));
+    }
+    return m;
+}
+
+template <class S, int P, int QX>
+cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                           int accumulate, int batch, cudaStream_t st) {
+    const char* s = getenv("IGALR_YRES");
+    const bool force_off = s && s[0] == '0';
+    const char* t = getenv("IGALR_TMA");
+    // TMA needs 16-byte row strides (even nx), 16-byte aligned input and the driver entry point
+    // bulk copies need 16-byte aligned coefficient rows: (factor * nx + x0) * BW even <=> nx even
+    const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0);
+    const bool yres = !force_off && yres_fits<S, P, QX>(pl.canon_nrounds);
+    if (tma) {
+        if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st);
+        return launch_canon_t<S, P, QX, false, true>(op, pl, src, dst, scale, accumulate, batch, st);
+    }
+    if (yres) return launch_canon_t<S, P, QX, true, false>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_t<S, P, QX, false, false>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+
+}  // namespace
+
+// Per-degree instantiations live in canon_p3.cu / canon_p4.cu (parallel compilation).
+cudaError_t canon_launch_p3(int part, const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                            int accumulate, int batch, cudaStream_t st);
+cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                            int accumulate, int batch, cudaStream_t st);
+
+#ifdef IGALR_CANON_P
+template <class S, int P>
+cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                             int accumulate, int batch, cudaStream_t st) {
+    const int qx = pick_qx(op->m[0], op->m[1], P);
+    if (qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+#define IGALR_CAT2(a, b) a##b
+#define IGALR_CAT(a, b) IGALR_CAT2(a, b)
+cudaError_t IGALR_CAT(canon_launch_p, IGALR_CANON_P)(int part, const iga_lr_op* op, const Plan& pl, const double* src,
+                                                     double* dst, double scale, int accumulate, int batch, cudaStream_t st) {
+    if (part == 0)
+        return launch_canon_deg<f2::ShapeMass, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_deg<f2::ShapeStiffA, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+}
+#endif
+
+#ifndef IGALR_CANON_P
+namespace {
+
+template <class S>
+iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
+    std::vector<f2::RoundC<S>> v;
+    if (!build_canon<S>(op, *pl, &v)) return IGA_EUNSUPPORTED;
+    const int n = (int)v.size();
+    if (canon_smem<S>(op->p[0], n) > 227 * 1024) return IGA_EUNSUPPORTED;
+    cudaError_t e = cudaMalloc(&pl->d_canon, sizeof(v[0]) * n);
+    if (e) return cuda_error(e, "cudaMalloc(canon rounds)");
+    e = cudaMemcpy(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice);
+    if (e) return cuda_error(e, "canon rounds H2D");
+    pl->canon_nrounds = n;
+    pl->canon_ok = true;
+    return IGA_OK;
+}
+
+}  // namespace
+
+iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part) {
+    if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
+    return part == 0 ? prepare_canon_t<f2::ShapeMass>(op, pl) : prepare_canon_t<f2::ShapeStiffA>(op, pl);
+}
+
+iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                            int accumulate, int batch, cudaStream_t st) {
+    cudaError_t e = op->p[0] == 3 ? canon_launch_p3(part, op, pl, src, dst, scale, accumulate, batch, st)
+                                  : canon_launch_p4(part, op, pl, src, dst, scale, accumulate, batch, st);
+    if (e) return cuda_error(e, "k_canon");
+    return IGA_OK;
+}
+
+namespace {
+}  // namespace
+
+bool fused2_supported(const iga_lr_op* op) {
+    if (op->p[0] != op->p[1] || op->p[0] != op->p[2]) return false;
+    return op->p[0] == 3 || op->p[0] == 4;
+}
+
+bool fused2_preferred(const iga_lr_op* op, int batch) {
+    // 128-wide tiles: narrow meshes waste lanes; small meshes cannot fill the persistent grid
+    // persistent CTAs need enough (tile, plane) units to fill the GPU
+    const long long N = (long long)op->m[0] * op->m[1] * op->m[2] * batch;
+    const char* s = getenv("IGALR_F2_MIN");
+    const long long thr = s ? atoll(s) : 0;
+    return N >= thr;
+}
+
+iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part) {
+    if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
+    size_t bytes = 0;
+    std::vector<char> blob;
+    if (part == 0) {
+        std::vector<f2::Round2<kMX, kMP, kMG>> v;
+        if (!build_rounds2<kMX, kMP, kMG, kMY>(*pl, &v)) return IGA_EUNSUPPORTED;
+        bytes = sizeof(v[0]) * v.size();
+        blob.assign((const char*)v.data(), (const char*)v.data() + bytes);
+        pl->f2_nrounds = (int)v.size();
+    } else {
+        std::vector<f2::Round2<kSX, kSP, kSG>> v;
+        if (!build_rounds2<kSX, kSP, kSG, kSY>(*pl, &v)) return IGA_EUNSUPPORTED;
+        bytes = sizeof(v[0]) * v.size();
+        blob.assign((const char*)v.data(), (const char*)v.data() + bytes);
+        pl->f2_nrounds = (int)v.size();
+    }
+    // shared memory budget
+    size_t sm = 0;
+    if (op->p[0] == 3)
+        sm = part ? f2::smem_bytes<3, rows_per_thread<3>(), kSX, kSP, kSG, kSY>(pl->f2_nrounds)
+                  : f2::smem_bytes<3, rows_per_thread<3>(), kMX, kMP, kMG, kMY>(pl->f2_nrounds);
+    else
+        sm = part ? f2::smem_bytes<4, rows_per_thread<4>(), kSX, kSP, kSG, kSY>(pl->f2_nrounds)
+                  : f2::smem_bytes<4, rows_per_thread<4>(), kMX, kMP, kMG, kMY>(pl->f2_nrounds);
+    if (sm > 227 * 1024) return IGA_EUNSUPPORTED;
+    cudaError_t e = cudaMalloc(&pl->d_f2, bytes);
+    if (e) return cuda_error(e, "cudaMalloc(f2 rounds)");
+    e = cudaMemcpy(pl->d_f2, blob.data(), bytes, cudaMemcpyHostToDevice);
+    if (e) return cuda_error(e, "f2 rounds H2D");
+    pl->f2_ok = true;
+    return IGA_OK;
+}
+
+iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
+                             int accumulate, int batch, cudaStream_t st) {
+    cudaError_t e = cudaErrorInvalidValue;
+    if (op->p[0] == 3) e = launch_part<3>(op, pl, part, src, dst, scale, accumulate, batch, st);
+    else if (op->p[0] == 4) e = launch_part<4>(op, pl, part, src, dst, scale, accumulate, batch, st);
+    if (e) return cuda_error(e, "k_fused2");
+    return IGA_OK;
+}
+
+#endif  // !IGALR_CANON_P
+
+}  // namespace igalr
