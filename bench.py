@@ -207,10 +207,49 @@ def op_kkt_flops(op) -> float:
 
 
 def launches_per_step(info: dict, path: str, kkt: bool) -> int:
+    """Our kernels per step: fused v2 = (k_canon + k_fixup) per part; KKT = k_kkt_combos + 3 applies
+    (2 parts, 2 parts, 1 part)."""
+    if info.get("fused2_ok") and path != "unfused":
+        return 1 + 2 * (2 + 2 + 1) if kkt else 4
     if info["fused_ok"] and path != "unfused":
         return 4 if kkt else 1
     r = info["n_rounds"]
     return (1 + 3 * 3 * r) if kkt else 3 * r
+
+
+def time_dominant_kernel(res, steps: int, path: str):
+    """The dominant kernel of the step is the stiffness k_canon (+ its boundary fixup): time a
+    stiffness-only apply with CUDA events on the launching stream; algorithmic flops = plan flops
+    of the stiffness part x batch."""
+    import torch
+    cfg, op, stream = res["cfg"], res["op"], res["stream"]
+    if cfg.kkt:
+        return None
+    x = torch.from_numpy(res["x"]).cuda()
+    ys = torch.empty_like(x)
+    for _ in range(3):
+        op.apply(x, None, ys, path=path, stream=stream)
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(5, min(steps, 50))
+    e0.record(stream)
+    for _ in range(n):
+        op.apply(x, None, ys, path=path, stream=stream)
+    e1.record(stream)
+    stream.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    flops = cfg.batch * res["info"]["plan_flops_stiff"]
+    return {"kernel": "k_canon<ShapeStiffA> + k_fixup (stiffness part)", "ms": ms, "flops": flops}
+
+
+def measured_traffic(workload: str):
+    """dram__bytes_read+write per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t.get(workload)
+    except Exception:
+        return None
 
 
 # ----------------------------------------------------------------------------------- CPU arm
@@ -278,8 +317,13 @@ def main():
     cfg = res["cfg"]
     ms = res["ms"]
     value = ws * res["dof"] / (ms * 1e-3) / 1e9
-    achieved = res["flops"] / (ms * 1e-3) / 1e12
+    achieved_step = res["flops"] / (ms * 1e-3) / 1e12
     peak = PEAK_FP64_TFLOPS
+    dom = time_dominant_kernel(res, a.steps, a.path)
+    if dom:
+        achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+    else:
+        achieved = achieved_step
     launches = launches_per_step(res["info"], a.path, cfg.kkt)
     line = {
         "metric": "GDoF/s of fp64 low-rank Kronecker operator/KKT apply; % of roofline",
@@ -290,9 +334,15 @@ def main():
                    "global_batch": cfg.batch * ws, "parallelism": "dp%d (batch sharded, no collective)" % ws,
                    "path": a.path, "l2": "inputs (%.0f MB) larger than L2 (126 MB); no flush" % (res["x"].nbytes / 1e6)},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "note": "FP64 DFMA pipe; peak measured by tools/ubench (DFMA/DMMA 37.0 TF/s); achieved = "
-                             "plan algorithmic flops / CUDA-event step time"},
+                     "frac": achieved / peak, "traffic": measured_traffic(cfg.name),
+                     "kernel": dom["kernel"] if dom else "whole step",
+                     "kernel_ms": dom["ms"] if dom else ms,
+                     "step_achieved": achieved_step, "step_frac": achieved_step / peak,
+                     "note": "FP64 DFMA pipe (bound 'alu'); peak = measured DFMA/DMMA rate 37.0 TF/s "
+                             "(tools/ubench.cu, profiles/r01_ubench.md; nominal 37.2 at 1965 MHz). achieved = "
+                             "algorithmic flops (2*nnz per banded mode product, DESIGN.md 5.2) of the dominant "
+                             "kernel / its CUDA-event time; step_* = whole mass+stiffness step. traffic = "
+                             "ncu dram bytes per launch (profiles/traffic.json)"},
         "gpu_launches": launches * a.steps,
         "clocks": res["clocks"],
         "setup_ms": res["setup_ms"],
