@@ -1130,10 +1130,8 @@ cudaError_t launch_part(const iga_lr_op* op, const Plan& pl, int part, const dou
 template <class S>
 bool build_canon(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<S>>* out);
 
-template <>
-bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMass>>* out) {
-    (void)op;
-    constexpr int K = f2::ShapeMass::NX;
+template <int K>
+bool build_canon_mass(const Plan& pl, std::vector<f2::RoundC<f2::ShapeMassK<K>>>* out) {
     out->clear();
     std::vector<const Round*> terms;
     for (const Round& R : pl.rounds) {
@@ -1142,7 +1140,7 @@ bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector
     }
     if (terms.empty()) return false;
     for (size_t i = 0; i < terms.size(); i += K) {
-        f2::RoundC<f2::ShapeMass> C;
+        f2::RoundC<f2::ShapeMassK<K>> C;
         memset(&C, 0, sizeof C);
         for (int k = 0; k < K; ++k) {
             const bool real = i + k < terms.size();
@@ -1156,6 +1154,17 @@ bool build_canon<f2::ShapeMass>(const iga_lr_op* op, const Plan& pl, std::vector
         out->push_back(C);
     }
     return out->size() <= (size_t)f2::kMaxRounds2;
+}
+
+template <>
+bool build_canon<f2::ShapeMassK<4>>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMassK<4>>>* out) {
+    (void)op;
+    return build_canon_mass<4>(pl, out);
+}
+template <>
+bool build_canon<f2::ShapeMassK<3>>(const iga_lr_op* op, const Plan& pl, std::vector<f2::RoundC<f2::ShapeMassK<3>>>* out) {
+    (void)op;
+    return build_canon_mass<3>(pl, out);
 }
 
 template <>
@@ -1374,8 +1383,11 @@ cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* 
 #define IGALR_CAT(a, b) IGALR_CAT2(a, b)
 cudaError_t IGALR_CAT(canon_launch_p, IGALR_CANON_P)(int part, const iga_lr_op* op, const Plan& pl, const double* src,
                                                      double* dst, double scale, int accumulate, int batch, cudaStream_t st) {
-    if (part == 0)
-        return launch_canon_deg<f2::ShapeMass, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (part == 0) {
+        if (pl.canon_mk == 3)
+            return launch_canon_deg<f2::ShapeMassK<3>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+        return launch_canon_deg<f2::ShapeMassK<4>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+    }
     return launch_canon_deg<f2::ShapeStiffA, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
 }
 #endif
@@ -1402,7 +1414,13 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
 
 iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part) {
     if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
-    return part == 0 ? prepare_canon_t<f2::ShapeMass>(op, pl) : prepare_canon_t<f2::ShapeStiffA>(op, pl);
+    if (part == 0) {
+        // mass terms per sweep: 4, or 3 when that avoids zero-padding terms (e.g. R = 6)
+        const int R = (int)pl->rounds.size();
+        pl->canon_mk = (R % 4 != 0 && R % 3 == 0) ? 3 : 4;
+        return pl->canon_mk == 3 ? prepare_canon_t<f2::ShapeMassK<3>>(op, pl) : prepare_canon_t<f2::ShapeMassK<4>>(op, pl);
+    }
+    return prepare_canon_t<f2::ShapeStiffA>(op, pl);
 }
 
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,

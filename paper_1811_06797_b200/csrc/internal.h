@@ -73,6 +73,7 @@ struct Plan {
     void* d_canon = nullptr;        // canonical-shape round tables (apply_fused2.cu)
     int canon_nrounds = 0;
     bool canon_ok = false;
+    int canon_mk = 4;               // mass terms per sweep of the canonical mass shape
 };
 enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kPlanF2Mass = 4, kPlanF2Stiff = 5, kNumPlans = 6 };
 }  // namespace igalr
