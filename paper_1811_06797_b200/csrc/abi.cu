@@ -566,11 +566,21 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     double* abc = nullptr;  // a, b, c combos [3][n_t][N]
     cudaError_t e = cudaMallocAsync(&abc, sizeof(double) * 3 * blk, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
-    iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);
-    // r_y = M b + tau S lambda ; r_u = tau M a ; r_lambda = M c + tau S y
-    if (!s) s = iga_lr_apply2(op, abc + blk, in + 2 * blk, out, 1.0, tau, n_t, flags, stream);
-    if (!s) s = iga_lr_apply2(op, abc, nullptr, out + blk, tau, 0.0, n_t, flags, stream);
-    if (!s) s = iga_lr_apply2(op, abc + 2 * blk, in, out + 2 * blk, 1.0, tau, n_t, flags, stream);
+    iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);  // abc = [b, tau a, c]
+    const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
+                       !(getenv("IGALR_F2_GENERIC") && getenv("IGALR_F2_GENERIC")[0] == '1');
+    if (!s && canon) {
+        // (r_y, r_u, r_lam) = M [b, tau a, c] in one launch over 3 n_t vectors, then
+        // r_y += tau S lambda and r_lam += tau S y (accumulating launches)
+        s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
+        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, n_t, st);
+        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
+    } else if (!s) {
+        // r_y = M b + tau S lambda ; r_u = tau M a ; r_lambda = M c + tau S y
+        s = iga_lr_apply2(op, abc, in + 2 * blk, out, 1.0, tau, n_t, flags, stream);
+        if (!s) s = iga_lr_apply2(op, abc + blk, nullptr, out + blk, 1.0, 0.0, n_t, flags, stream);
+        if (!s) s = iga_lr_apply2(op, abc + 2 * blk, in, out + 2 * blk, 1.0, tau, n_t, flags, stream);
+    }
     cudaFreeAsync(abc, st);
     return s;
 }

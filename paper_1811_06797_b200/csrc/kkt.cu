@@ -6,7 +6,9 @@
 //   r_u[k]   = tau beta M u_k - tau M lambda_k                   = tau M a_k
 //   r_lam[k] = (M + tau S) y_k - M y_{k-1} - tau M u_k          = M c_k + tau S y_k
 // with a_k = beta u_k - lambda_k,  b_k = tau y_k + lambda_k - lambda_{k+1},
-//      c_k = y_k - y_{k-1} - tau u_k.  This kernel forms a, b, c.
+//      c_k = y_k - y_{k-1} - tau u_k.  This kernel forms them as
+// [b, tau*a, c] so that one mass apply over a batch of 3*n_t vectors writes (r_y, r_u, r_lam)
+// = (M b, tau M a, M c) directly into the output blocks; the two stiffness terms accumulate.
 #include "internal.h"
 
 namespace igalr {
@@ -22,9 +24,9 @@ __global__ void k_kkt_combos(const double* __restrict__ in, double* __restrict__
         const double yk = y[g], uk = u[g], lk = l[g];
         const double lnext = (k + 1 < n_t) ? l[g + N] : 0.0;
         const double yprev = (k >= 1) ? y[g - N] : 0.0;
-        abc[g] = beta * uk - lk;
-        abc[blk + g] = tau * yk + lk - lnext;
-        abc[2 * blk + g] = yk - yprev - tau * uk;
+        abc[g] = tau * yk + lk - lnext;             // b_k
+        abc[blk + g] = tau * (beta * uk - lk);      // tau * a_k
+        abc[2 * blk + g] = yk - yprev - tau * uk;   // c_k
     }
 }
 
