@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libigalr.so")
+LIB_PATH = (os.environ.get("IGALR_LIB") or os.path.join(_HERE, "libigalr.so"))  # override: experiments only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

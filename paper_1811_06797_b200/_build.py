@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-LIB = os.path.join(HERE, "libigalr.so")
-BUILD = os.path.join(ROOT, "build", "igalr")
+LIB = os.environ.get("IGALR_LIB_OUT", os.path.join(HERE, "libigalr.so"))
+BUILD = os.environ.get("IGALR_BUILD_DIR", os.path.join(ROOT, "build", "igalr"))
+EXTRA = os.environ.get("IGALR_NVCC_EXTRA", "").split()  # experiment defines (never set for the product)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -39,7 +40,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, s + ".o")
         objs.append(obj)
         if force or _newer([src] + headers + [__file__], obj):
-            cmd = [NVCC] + ARCH + FLAGS + ["-I" + INCLUDE, "-I" + CSRC, "-c", src, "-o", obj]
+            cmd = [NVCC] + ARCH + FLAGS + EXTRA + ["-I" + INCLUDE, "-I" + CSRC, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             jobs.append(cmd)

@@ -439,6 +439,7 @@ void iga_lr_destroy(iga_lr_op* op) {
         release_fused(&op->plan[k]);
         if (op->plan[k].d_f2) cudaFree(op->plan[k].d_f2);
         if (op->plan[k].d_canon) cudaFree(op->plan[k].d_canon);
+        if (op->plan[k].d_ztab) cudaFree(op->plan[k].d_ztab);
     }
     delete op;
 }

@@ -57,7 +57,8 @@ struct Args2 {
     double* scratch;       // [nctas][NSEG][4P][L][TX] partial planes
     const double* bx;
     const double* by;
-    const double* bz;
+    const double* bz;      // z-factor bands; on the GSYNC canonical path instead the per-plane z
+                           // records [mz][nrounds][NGB] (slot-permuted, group-scaled; k_build_ztab)
     const void* rounds;
     int nrounds;
     int mx, my, mz, batch;
@@ -577,8 +578,21 @@ struct GeoC {
     static constexpr int BWP = (BW + 1) & ~1;     // y-coef row pitch (16-byte aligned rows)
     static constexpr int HY = TY + 2 * P;
     static constexpr int HX = TXT_ + 2 * P;
-    static constexpr int HXP = HX + 1;
+    // plane rows: smem column c holds global column x0 - P - PADL + c, so that (nx even) row
+    // segments start 16-byte aligned in global and shared memory (bulk copies); even pitch
+    static constexpr int PADL = P & 1;
+    static constexpr int HXP = (HX + PADL + 1) & ~1;
 };
+template <int NG, int BW>
+struct ZPitch {
+    static constexpr int NGB = (NG * BW + 1) & ~1;  // z-coefficients per round, 16-byte multiple
+};
+
+// Group-synchronised rounds + bulk-copied plane rows (needs bulk copies and resident y).
+template <int P, bool TMA, bool YRES>
+__host__ __device__ constexpr bool gsync_path() {
+    return TMA && YRES;
+}
 
 // QX of the 4 TMEM lane quadrants tile x (32 columns each); the other 4/QX stack in y.
 template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA>
@@ -587,7 +601,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
     using G_ = GeoC<P, TX, TY>;
     constexpr int BW = G_::BW, BWP = G_::BWP, HY = G_::HY;
-    constexpr int HXP = G_::HXP;
+    constexpr int HXP = G_::HXP, PADL = G_::PADL;
     constexpr int VSZ = (HY * G_::HXP + 15) & ~15;  // doubles per plane buffer (128-B aligned)
     constexpr int NX = S::NX, NY = S::NY, NG = S::NG, NPAIR = S::NPAIR;
     using RS = RingShape<BW>;
@@ -601,15 +615,25 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     constexpr int YSLOTS = YRES ? 0 : 2;
     const int nyslots = YRES ? a.nrounds : YSLOTS;
     double* ycs = xcs + 2 * NX * TX * BW;               // [nyslots][NY][TY][BWP]
-    double* zcs = ycs + (size_t)nyslots * NY * TY * BWP;  // [2][nrounds][NG][BW] (per plane)
-    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NG * BW);
+    constexpr int NGB = ZPitch<NG, BW>::NGB;
+    double* zcs = ycs + (size_t)nyslots * NY * TY * BWP;  // [2][nrounds][NGB] (per plane)
+    RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NGB);
     __shared__ uint32_t tmem_base_sh;
-    __shared__ __align__(8) uint64_t xbar[2];  // bulk-copy completion of the x-coefficient buffers
-    uint32_t xph[2] = {0, 0};
+    // bulk-copy completion of the x-coefficient buffers, per column group (GSYNC) or CTA-wide
+    __shared__ __align__(8) uint64_t xbar[QX][2];
+    __shared__ __align__(8) uint64_t pbar[2];  // GSYNC: plane rows + z record landed
+    uint32_t xph = 0, pph = 0;  // mbarrier parity per buffer (bit b: buffer b; no local-memory arrays)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int quad = warp & 3, sub = warp >> 2;
     const int cx = (quad % QX) * TXW + lane;                 // tile column of this thread
+    // GSYNC: the warps of one column group (same quad % QX: 32 columns) are the only readers of
+    // the group's x-coefficients, so rounds are separated by a group barrier (named barrier
+    // 1 + grp) and only the first round of a plane (new plane buffer) by a CTA barrier.
+    constexpr bool GSYNC = gsync_path<P, TMA, YRES>();
+    const int grp = GSYNC ? quad % QX : 0;
+    constexpr int GTHREADS = GSYNC ? 32 * WPQ * (4 / QX) : NW * WPQ * 32;
+    const bool gprod = GSYNC ? (warp == grp && lane == 0) : (threadIdx.x == 0);  // x-copy issuer
     const int row0 = ((quad / QX) * WPQ + sub) * LW;          // first tile output row of this warp
 
     if (warp == 0) {
@@ -619,7 +643,9 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     for (int i = threadIdx.x; i < a.nrounds * (int)(sizeof(RoundT) / 4); i += blockDim.x)
         reinterpret_cast<int*>(rs)[i] = reinterpret_cast<const int*>(a.rounds)[i];
     if (TMA && threadIdx.x == 0) {
-        for (int k = 0; k < 2; ++k) mbar_init(&xbar[k], 1);
+        for (int g = 0; g < QX; ++g)
+            for (int k = 0; k < 2; ++k) mbar_init(&xbar[g][k], 1);
+        for (int k = 0; k < 2; ++k) mbar_init(&pbar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -646,6 +672,12 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         const int gx = x0 + cx;
 
         __syncthreads();
+        if constexpr (GSYNC) {
+            // halo zeros: the plane bulk copies only ever write in-range rows and columns
+            for (int i = threadIdx.x; i < 2 * VSZ; i += blockDim.x) vin[i] = 0.0;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+        }
         if constexpr (YRES) {
             for (int r = 0; r < a.nrounds; ++r) {
                 const RoundT& R = rs[r];
@@ -666,6 +698,25 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         }
 
         auto stage_plane = [&](int zp, int buf) {
+            if constexpr (GSYNC) {
+                // one thread: the in-range part of every tile row (widened to an even, 16-byte
+                // aligned column range) and the plane's z record, completing on pbar[buf]
+                if (threadIdx.x == 0) {
+                    const int cbase = x0 - P - PADL;
+                    const int cs = max(cbase, 0);
+                    const int ce = min((min(x0 + TX + P, a.mx) + 1) & ~1, a.mx);
+                    const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
+                    const uint32_t rb = (uint32_t)((ce - cs) * sizeof(double));
+                    const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
+                    mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
+                    double* dstp = vin + buf * VSZ + (cs - cbase);
+                    const double* srcp = a.src + vb + (long long)zp * plane + cs;
+                    for (int r = rlo; r < rhi; ++r)
+                        bulk_g2s(dstp + r * HXP, srcp + (long long)(y0 - P + r) * a.mx, rb, &pbar[buf]);
+                    bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes, &pbar[buf]);
+                }
+                return;
+            }
             double* dstp = vin + buf * VSZ;
             const double* srcp = a.src + vb + (long long)zp * plane;
             {
@@ -680,18 +731,18 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     for (int c = lane; c < G_::HX; c += 32) {
                         const int gxx = x0 - P + c;
                         const bool ok = rowok && gxx >= 0 && gxx < a.mx;
-                        cp8(dstp + r * HXP + c, ok ? srow + c : a.src, ok);
+                        cp8(dstp + r * HXP + PADL + c, ok ? srow + c : a.src, ok);
                     }
                 }
             }
-            double* zdst = zcs + buf * a.nrounds * NG * BW;
+            double* zdst = zcs + buf * a.nrounds * NGB;
             for (int i = threadIdx.x; i < a.nrounds * NG * BW; i += blockDim.x) {
                 const int r = i / (NG * BW), rem = i - r * NG * BW;
                 const int g = rem / BW, j = rem - g * BW;
                 const RoundT& R = rs[r];
                 const int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;
                 const bool ok = zo >= 0 && zo < a.mz;
-                cp8(zdst + i, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
+                cp8(zdst + r * NGB + rem, ok ? a.bz + ((size_t)R.gf[g] * a.mz + zo) * BW + (zp - zo + P) : a.bz, ok);
             }
         };
         auto stage_xc = [&](int r, int buf) {
@@ -700,13 +751,23 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             // are never used for an output)
             const RoundT& R = rs[r];
             double* dstp = xcs + buf * NX * TX * BW;
-            if constexpr (TMA) {
+            if constexpr (GSYNC) {
+                // the column group's 32 columns of every x-entry
+                if (gprod) {
+                    mbar_expect_tx(&xbar[grp][buf], (uint32_t)(NX * TXW * BW * sizeof(double)));
+#pragma unroll
+                    for (int e = 0; e < NX; ++e)
+                        bulk_g2s(dstp + e * TX * BW + grp * TXW * BW,
+                                 a.bx + ((size_t)R.xf[e] * a.mx + x0 + grp * TXW) * BW,
+                                 (uint32_t)(TXW * BW * sizeof(double)), &xbar[grp][buf]);
+                }
+            } else if constexpr (TMA) {
                 if (threadIdx.x == 0) {
-                    mbar_expect_tx(&xbar[buf], (uint32_t)(NX * TX * BW * sizeof(double)));
+                    mbar_expect_tx(&xbar[0][buf], (uint32_t)(NX * TX * BW * sizeof(double)));
 #pragma unroll
                     for (int e = 0; e < NX; ++e)
                         bulk_g2s(dstp + e * TX * BW, a.bx + ((size_t)R.xf[e] * a.mx + x0) * BW,
-                                 (uint32_t)(TX * BW * sizeof(double)), &xbar[buf]);
+                                 (uint32_t)(TX * BW * sizeof(double)), &xbar[0][buf]);
                 }
             } else {
 #pragma unroll
@@ -733,23 +794,41 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         for (int zp = za; zp < zb; ++zp) {
             for (int r = 0; r < a.nrounds; ++r) {
                 const bool last_round = (r == a.nrounds - 1);
-                if constexpr (TMA) {  // x-coefficients arrive by cp.async.bulk (mbarrier)
-                    mbar_wait(&xbar[xbuf], xph[xbuf]);
-                    xph[xbuf] ^= 1;
+                if constexpr (GSYNC) {
+                    tm_wait_st();
+                    if (r == 0) {  // new plane buffer: CTA barrier, then request plane z'+1
+                        cp_wait<0>();  // (resident y-coefficients at a segment start)
+                        __syncthreads();
+                        if (zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
+                        mbar_wait(&pbar[pbuf], (pph >> pbuf) & 1);
+                        pph ^= 1u << pbuf;
+                    } else {
+                        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(GTHREADS) : "memory");
+                    }
+                    // the group is past round r-1: its x buffer can take round r+1
+                    if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                    else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                    mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
+                    xph ^= 1u << xbuf;
+                } else {
+                    if constexpr (TMA) {  // x-coefficients arrive by cp.async.bulk (mbarrier)
+                        mbar_wait(&xbar[0][xbuf], (xph >> xbuf) & 1);
+                        xph ^= 1u << xbuf;
+                    }
+                    cp_wait<0>();
+                    tm_wait_st();
+                    __syncthreads();
+                    if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                    else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                    if (r == 0 && zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
+                    cp_commit();
                 }
-                cp_wait<0>();
-                tm_wait_st();
-                __syncthreads();
-                if (!last_round) stage_xc(r + 1, xbuf ^ 1);
-                else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
-                if (r == 0 && zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
-                cp_commit();
 
                 const RoundT& R = rs[r];
-                const double* vt = vin + pbuf * VSZ + row0 * HXP + cx;
+                const double* vt = vin + pbuf * VSZ + row0 * HXP + PADL + cx;
                 const double* xc = xcs + xbuf * NX * TX * BW;
                 const double* yc = ycs + (size_t)(YRES ? r : xbuf) * NY * TY * BWP + (size_t)row0 * BWP;
-                const double* zc = zcs + pbuf * a.nrounds * NG * BW + r * NG * BW;
+                const double* zc = zcs + pbuf * a.nrounds * NGB + r * NGB;
                 double xr[NX][BW];
 #pragma unroll
                 for (int e = 0; e < NX; ++e)
@@ -758,7 +837,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 double zr[NG][BW];
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
-                    const double gsc = R.gs[g];
+                    const double gsc = GSYNC ? 1.0 : R.gs[g];  // (the GSYNC z record is pre-scaled)
 #pragma unroll
                     for (int j = 0; j < BW; ++j) zr[g][j] = zc[g * BW + j] * gsc;
                 }
@@ -799,7 +878,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     constexpr int Q = decltype(Qc)::value;
                     const uint32_t tp = tbase + i * RS::COLS;
                     uint32_t rr[RS::DBL * 2];
-                    ring_issue<BW>(tp, rr);  // TMEM load in flight during the Y stage
+                    // TMEM load in flight during the Y stage (p=3); p=4 issues it after the Y stage:
+                    // its 18 registers would push the Y stage into spills
+                    constexpr bool EARLY_RING = (P <= 3);
+                    if constexpr (EARLY_RING) ring_issue<BW>(tp, rr);
                     double G[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) G[g] = 0.0;
@@ -827,11 +909,13 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                                 double u = yv[0] * w[e][(Q + 1) % BW];
 #pragma unroll
                                 for (int k = 1; k < BW; ++k) u = fma(yv[k], w[e][(Q + 1 + k) % BW], u);
-                                G[g] = fma(pc[j], u, G[g]);
+                                // (p=4: the ratio is re-read from shared memory: register pressure)
+                                G[g] = fma(P <= 3 ? pc[j] : R.pc[j], u, G[g]);
                             }
                         }
                     }
                     double ring[RS::DBL];
+                    if constexpr (!EARLY_RING) ring_issue<BW>(tp, rr);
                     ring_wait<BW>(rr, ring);
 #pragma unroll
                     for (int g = 0; g < NG; ++g)
@@ -929,7 +1013,7 @@ size_t smem_bytes_canon(int nrounds) {
     const size_t ys = YRES ? (size_t)nrounds : 2;
     const size_t vsz = (G_::HY * G_::HXP + 15) & ~(size_t)15;
     return sizeof(double) * (2 * vsz + 2 * S::NX * TXT * G_::BW + ys * S::NY * TYT * G_::BWP +
-                             2 * (size_t)nrounds * S::NG * G_::BW) +
+                             2 * (size_t)nrounds * ZPitch<S::NG, G_::BW>::NGB) +
            sizeof(RoundC<S>) * nrounds + 64;
 }
 
@@ -1285,6 +1369,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     a.by = op->F[1].band;
     a.bz = op->F[2].band;
     a.rounds = pl.d_canon;
+    if (gsync_path<P, TMA, YRES>()) a.bz = pl.d_ztab;  // GSYNC path: per-plane z records
     a.nrounds = pl.canon_nrounds;
     a.mx = op->m[0];
     a.my = op->m[1];
@@ -1352,7 +1437,8 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     const char* t = getenv("IGALR_TMA");
     // TMA needs 16-byte row strides (even nx), 16-byte aligned input and the driver entry point
     // bulk copies need 16-byte aligned coefficient rows: (factor * nx + x0) * BW even <=> nx even
-    const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0);
+    // the GSYNC path (TMA && YRES) also bulk-copies plane rows: 16-byte aligned input
+    const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
     const bool yres = !force_off && yres_fits<S, P, QX>(pl.canon_nrounds);
     if (tma) {
         if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st);
@@ -1395,6 +1481,27 @@ cudaError_t IGALR_CAT(canon_launch_p, IGALR_CANON_P)(int part, const iga_lr_op* 
 #ifndef IGALR_CANON_P
 namespace {
 
+// Per-plane z-coefficient records of the GSYNC canonical kernel (one bulk copy per plane):
+//   ztab[z'][r][g*BW + j] = gs_r[g] * Fz_{gf_r[g]}[zo][z' - zo + P],  zo = the output plane held in
+// ring slot j while input plane z' is processed (zo = z' - P + ((j - (z' - P)) mod BW)), 0 if zo is
+// outside the mesh; entries j >= NG*BW (record padding to 16 bytes) are 0.
+__global__ void k_build_ztab(const double* __restrict__ bz, const int* __restrict__ gf, const double* __restrict__ gs,
+                             int nrounds, int ng, int ngb, int mz, int P, double* __restrict__ ztab) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)mz * nrounds * ngb) return;
+    const int BW = 2 * P + 1;
+    const int q = (int)(i % ngb);
+    const int r = (int)((i / ngb) % nrounds);
+    const int zp = (int)(i / ((long long)ngb * nrounds));
+    double v = 0.0;
+    if (q < ng * BW) {
+        const int g = q / BW, j = q % BW;
+        const int zo = zp - P + ((j - (zp - P)) % BW + BW) % BW;
+        if (zo >= 0 && zo < mz) v = gs[r * ng + g] * bz[((size_t)gf[r * ng + g] * mz + zo) * BW + (zp - zo + P)];
+    }
+    ztab[i] = v;
+}
+
 template <class S>
 iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
     std::vector<f2::RoundC<S>> v;
@@ -1405,6 +1512,32 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
     if (e) return cuda_error(e, "cudaMalloc(canon rounds)");
     e = cudaMemcpy(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice);
     if (e) return cuda_error(e, "canon rounds H2D");
+    // per-plane z records (GSYNC path)
+    const int P = op->p[2], BW = 2 * P + 1, mz = op->m[2];
+    const int ngb = (S::NG * BW + 1) & ~1;
+    std::vector<int> gf(n * S::NG);
+    std::vector<double> gs(n * S::NG);
+    for (int r = 0; r < n; ++r)
+        for (int g = 0; g < S::NG; ++g) {
+            gf[r * S::NG + g] = v[r].gf[g];
+            gs[r * S::NG + g] = v[r].gs[g];
+        }
+    int* d_gf = nullptr;
+    double* d_gs = nullptr;
+    const size_t nz = (size_t)mz * n * ngb;
+    e = cudaMalloc(&pl->d_ztab, sizeof(double) * nz);
+    if (!e) e = cudaMalloc(&d_gf, sizeof(int) * gf.size());
+    if (!e) e = cudaMalloc(&d_gs, sizeof(double) * gs.size());
+    if (!e) e = cudaMemcpy(d_gf, gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(d_gs, gs.data(), sizeof(double) * gs.size(), cudaMemcpyHostToDevice);
+    if (!e) {
+        k_build_ztab<<<(unsigned)((nz + 255) / 256), 256>>>(op->F[2].band, d_gf, d_gs, n, S::NG, ngb, mz, P, pl->d_ztab);
+        e = cudaGetLastError();
+    }
+    if (!e) e = cudaDeviceSynchronize();
+    cudaFree(d_gf);
+    cudaFree(d_gs);
+    if (e) return cuda_error(e, "canon z records");
     pl->canon_nrounds = n;
     pl->canon_ok = true;
     return IGA_OK;

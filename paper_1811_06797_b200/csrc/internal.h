@@ -71,6 +71,7 @@ struct Plan {
     int f2_nrounds = 0;
     bool f2_ok = false;
     void* d_canon = nullptr;        // canonical-shape round tables (apply_fused2.cu)
+    double* d_ztab = nullptr;       // per-plane z records of the canonical kernel (GSYNC path)
     int canon_nrounds = 0;
     bool canon_ok = false;
     int canon_mk = 4;               // mass terms per sweep of the canonical mass shape
