@@ -1077,6 +1077,102 @@ static __global__ void k_fixup(const Args2 a, int P, int L) {
     }
 }
 
+// k_fixup for the canonical kernels (tile TY x TX, TX a multiple of 4): the same contributor
+// search and summation order, with each thread summing 4 consecutive points per step and all
+// partial loads of a thread issued before its stores (the plane-sized loop is latency-bound).
+static __global__ void __launch_bounds__(256) k_fixup4(const Args2 a, int P) {
+    __shared__ int s_valid, s_n, s_b, s_zo, s_txi, s_tyi;
+    __shared__ long long s_off[8];
+    const int kb = 1 + blockIdx.x / (2 * P);
+    const int s = blockIdx.x % (2 * P);
+    const int TY = a.tyt, TX = a.txt;
+    if (threadIdx.x == 0) {
+        s_valid = 0;
+        s_n = 0;
+        const long long ub = unit_begin(kb, a.units, a.nctas);
+        const long long tile = ub / a.mz;
+        const int zbnd = (int)(ub - tile * a.mz);
+        const int zo = zbnd - P + s;
+        if (zbnd != 0 && zo >= 0 && zo < a.mz) {
+            long long tt = tile;
+            s_txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+            s_tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+            s_b = (int)tt;
+            s_zo = zo;
+            const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
+            const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
+            long long k0 = kb - 1, k1 = kb;
+            while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
+            while (k1 + 1 < a.nctas && unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
+            for (long long k = k0; k <= k1 && s_n < 8; ++k) {
+                const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
+                int seg = 0;
+                for (long long u = cu0; u < cu1; ++seg) {
+                    const long long t2 = u / a.mz;
+                    const int sa = (int)(u - t2 * a.mz);
+                    const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
+                    if (t2 == tile) {
+                        const int slot = partial_slot(zo, sa, sb, P);
+                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)TY * TX;
+                        break;
+                    }
+                    u += sb - sa;
+                }
+            }
+            s_valid = 1;
+        }
+    }
+    __syncthreads();
+    if (!s_valid) return;
+    const long long plane = (long long)a.mx * a.my;
+    const long long obase = (long long)s_b * a.mz * plane + (long long)s_zo * plane;
+    const int n = s_n;
+    const int nq = TY * TX / 4;
+    for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * blockDim.x) {
+        double4 acc[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[t] = make_double4(0.0, 0.0, 0.0, 0.0);
+        for (int c = 0; c < n; ++c) {
+            const double2* src = reinterpret_cast<const double2*>(a.scratch + s_off[c]);
+            double2 v[4][2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int q = q0 + t * blockDim.x;
+                if (q < nq) {
+                    v[t][0] = __ldcg(src + 2 * q);
+                    v[t][1] = __ldcg(src + 2 * q + 1);
+                } else {
+                    v[t][0] = v[t][1] = make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                acc[t].x += v[t][0].x;
+                acc[t].y += v[t][0].y;
+                acc[t].z += v[t][1].x;
+                acc[t].w += v[t][1].y;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int q = q0 + t * blockDim.x;
+            if (q >= nq) continue;
+            const int p = 4 * q;
+            const int i = p / TX, cx = p - i * TX;
+            const int gy = s_tyi * TY + i;
+            if (gy >= a.my) continue;
+            const double vv[4] = {acc[t].x, acc[t].y, acc[t].z, acc[t].w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int gx = s_txi * TX + cx + w;
+                if (gx >= a.mx) continue;
+                const long long o = obase + (long long)gy * a.mx + gx;
+                a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + vv[w];
+            }
+        }
+    }
+}
+
 template <int P, int L, int NX, int NP, int NG, int NY>
 size_t smem_bytes(int nrounds) {
     using G_ = Geo<P, L>;
@@ -1401,7 +1497,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a, tmap);
     e = cudaGetLastError();
     if (!e && a.nctas > 1) {
-        k_fixup<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P, TYT);
+        k_fixup4<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
