@@ -125,6 +125,29 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
 iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in,
                          double* out, uint32_t flags, void* stream);
 
+/* ---------------------------------------------------------------- KKT solve (NEXT-1)
+   All-at-once solve of Eq. (KKTSystem) PAPER.md:313-319 for (y, u, lambda) by MINRES
+   (Paige & Saunders; the Krylov method the paper names for its reduced KKT systems,
+   PAPER.md:399-400), unpreconditioned, with iga_kkt_apply as the matvec.
+     rhs : DEVICE fp64 [3][n_t][Nz][Ny][Nx] (blocks y, u, lambda; e.g. [tau M yhat; 0; 0])
+     x   : DEVICE fp64, same layout.  On entry the initial guess if flags has IGA_MINRES_X0,
+           otherwise ignored (x_0 = 0); on return the last MINRES iterate.
+     rtol: stop when |r_j| <= rtol |r_0| (|r_j| from the MINRES recurrence, |eta|);
+     maxit: iteration cap (0 => only r_0 is formed).
+     flags: IGA_PATH_* (passed to the matvec) | IGA_MINRES_X0.
+   Workspace (5 vectors) is stream-ordered scratch; the call synchronises `stream` once per
+   iteration (8-byte read of |eta|) and before returning.  Reductions are deterministic.
+   Errors: as iga_kkt_apply, plus IGA_EINVAL for rhs == x, maxit < 0, rtol < 0. */
+#define IGA_MINRES_X0 0x100u
+typedef struct {
+    int32_t iters;      /* MINRES iterations performed */
+    int32_t converged;  /* 1 if |r| <= rtol |r_0| */
+    double relres;      /* |r_iters| / |r_0| (recurrence estimate) */
+    double res0;        /* |r_0| = |rhs - A x_0| */
+} iga_minres_info;
+iga_status iga_kkt_minres(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* rhs, double* x,
+                          double rtol, int32_t maxit, uint32_t flags, void* stream, iga_minres_info* info);
+
 /* End-to-end variants with HOST buffers (pageable or pinned): copy in, apply, copy out,
    synchronise `stream`.  Device staging is stream-ordered scratch owned by the call. */
 iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host,

@@ -18,6 +18,12 @@ What it computes (each function cites the passage it follows):
 * ``apply_rows``          the same bilinear forms for selected output rows.
 * ``kkt_apply``           Eq. (KKTSystem) PAPER.md:313-319 written as the paper's three
                           gradient rows PAPER.md:306-308 per time step.
+* ``kkt_dense``           the KKT matrix of Eq. (KKTSystem) assembled block by block from the
+                          CSR M, S with calM = I (x) M, calK = I (x) tau S + C (x) M
+                          (PAPER.md:316-318), for small sizes (dense LU solves, pins).
+* ``minres``              MINRES (Paige & Saunders), the recurrence of Elman-Silvester-Wathen
+                          Algorithm 2.4 with P = I, step by step (the Krylov method of
+                          PAPER.md:399-400; NEXT-1 of SURVEY.md §8(f)).
 
 Parity pins: tests/test_oracle_pins.py (P1-P12 of SURVEY.md §8(c)).
 Every function here is pinned; none is "parity unpinned".
@@ -310,3 +316,71 @@ def kkt_rows(P: Problem, X: np.ndarray, tau: float, beta: float, steps: Sequence
         res[1, j] = tau * beta * Mu - tau * Ml
         res[2, j] = My - My_prev + tau * Sy - tau * Mu
     return res
+
+
+def kkt_dense(M, S, n_t: int, tau: float, beta: float) -> np.ndarray:
+    """Dense KKT matrix of Eq. (KKTSystem) PAPER.md:313-319:
+        [[tau calM, 0, calK^T], [0, tau beta calM, -tau calM], [calK, -tau calM, 0]]
+    with calM = I_{n_t} (x) M and calK = I_{n_t} (x) tau S + C (x) M, C = 1 on the diagonal and
+    -1 on the first subdiagonal.  Block order (y, u, lambda), each block
+    time-major [n_t][N] like the GPU layout.  Small sizes only."""
+    Md = M.toarray() if hasattr(M, "toarray") else np.asarray(M)
+    Sd = S.toarray() if hasattr(S, "toarray") else np.asarray(S)
+    I = np.eye(n_t)
+    C = np.eye(n_t) - np.eye(n_t, k=-1)
+    calM = np.kron(I, Md)
+    calK = np.kron(I, tau * Sd) + np.kron(C, Md)
+    Z = np.zeros_like(calM)
+    return np.block([[tau * calM, Z, calK.T], [Z, tau * beta * calM, -tau * calM], [calK, -tau * calM, Z]])
+
+
+def minres(matvec, b: np.ndarray, x0: Optional[np.ndarray] = None, maxit: int = 1000, rtol: float = 1e-8):
+    """MINRES for symmetric A (Paige & Saunders 1975), in the form of Elman, Silvester & Wathen,
+    Algorithm 2.4, with P = I, written out step by step:
+
+        q_0 = 0, r_0 = b - A x_0, gamma_1 = |r_0|, q_1 = r_0 / gamma_1, eta = gamma_1,
+        c_0 = c_1 = 1, s_0 = s_1 = 0, w_0 = w_1 = 0;  for j = 1, 2, ...
+          delta_j = q_j' A q_j
+          r = A q_j - delta_j q_j - gamma_j q_{j-1};  gamma_{j+1} = |r|;  q_{j+1} = r / gamma_{j+1}
+          a0 = c_j delta_j - c_{j-1} s_j gamma_j;  a1 = sqrt(a0^2 + gamma_{j+1}^2)
+          a2 = s_j delta_j + c_{j-1} c_j gamma_j;  a3 = s_{j-1} gamma_j
+          c_{j+1} = a0 / a1;  s_{j+1} = gamma_{j+1} / a1
+          w_{j+1} = (q_j - a3 w_{j-1} - a2 w_j) / a1;  x_j = x_{j-1} + c_{j+1} eta w_{j+1}
+          eta = -s_{j+1} eta
+
+    Stops when |eta| <= rtol |r_0| or after maxit iterations.  Returns (x, iters, |eta|/|r_0|,
+    |r_0|).  Vectors are flat float64; `matvec` maps a flat vector to A times it."""
+    b = np.asarray(b, dtype=np.float64).ravel()
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64).ravel()
+    r = b - matvec(x) if x0 is not None else b.copy()
+    gamma = float(np.sqrt(r @ r))
+    res0 = gamma
+    q_prev = np.zeros_like(b)
+    q = r / gamma if gamma > 0 else np.zeros_like(b)
+    w_prev = np.zeros_like(b)
+    w = np.zeros_like(b)
+    eta = gamma
+    c_prev = c = 1.0
+    s_prev = s = 0.0
+    it = 0
+    while it < maxit and abs(eta) > rtol * res0:
+        Aq = matvec(q)
+        delta = float(Aq @ q)
+        r = Aq - delta * q - gamma * q_prev
+        gamma_next = float(np.sqrt(r @ r))
+        a0 = c * delta - c_prev * s * gamma
+        a1 = float(np.sqrt(a0 * a0 + gamma_next * gamma_next))
+        a2 = s * delta + c_prev * c * gamma
+        a3 = s_prev * gamma
+        c_next = a0 / a1 if a1 > 0 else 1.0
+        s_next = gamma_next / a1 if a1 > 0 else 0.0
+        w_next = (q - a3 * w_prev - a2 * w) / a1 if a1 > 0 else np.zeros_like(b)
+        x = x + (c_next * eta) * w_next
+        eta = -s_next * eta
+        q_prev, q = q, (r / gamma_next if gamma_next > 0 else np.zeros_like(b))
+        w_prev, w = w, w_next
+        c_prev, c = c, c_next
+        s_prev, s = s, s_next
+        gamma = gamma_next
+        it += 1
+    return x, it, (abs(eta) / res0 if res0 > 0 else 0.0), res0

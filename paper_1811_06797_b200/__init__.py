@@ -35,7 +35,8 @@ STATUS_NAMES = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_ENOMEM", 3: "IGA_ECUDA", 4
 
 ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "iga_lr_apply", "iga_lr_apply2",
                "iga_kkt_apply", "iga_lr_apply_host", "iga_kkt_apply_host", "iga_lr_info", "iga_lr_export_factor",
-               "iga_last_error", "iga_version"]
+               "iga_last_error", "iga_version", "iga_kkt_minres"]
+MINRES_X0 = 0x100
 
 
 class IgaError(RuntimeError):
@@ -66,6 +67,12 @@ class _Info(ctypes.Structure):
                 ("plan_flops_stiff", ctypes.c_double)]
 
 
+class MinresInfo(ctypes.Structure):
+    """iga_minres_info: iterations, convergence flag, |r|/|r_0| and |r_0| of iga_kkt_minres."""
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("relres", ctypes.c_double),
+                ("res0", ctypes.c_double)]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.POINTER(ctypes.c_double)
 _lib.iga_last_error.restype = ctypes.c_char_p
@@ -85,6 +92,8 @@ _lib.iga_lr_apply_host.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_dou
 _lib.iga_kkt_apply_host.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_uint32,
                                     _P]
 _lib.iga_lr_info.argtypes = [_P, ctypes.POINTER(_Info)]
+_lib.iga_kkt_minres.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_double,
+                                ctypes.c_int32, ctypes.c_uint32, _P, ctypes.POINTER(MinresInfo)]
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -246,6 +255,17 @@ class LowRankOperator:
         """out = KKT(tau, beta, n_t) X for device tensors [3, n_t, nz, ny, nx] (Eq. (KKTSystem))."""
         _check(_lib.iga_kkt_apply(self._h, int(n_t), float(tau), float(beta), _tensor_ptr(X, "X"),
                                   _tensor_ptr(out, "out"), PATHS[path], _stream_handle(stream)))
+
+    def kkt_minres(self, rhs, x, n_t: int, tau: float, beta: float, rtol: float = 1e-8, maxit: int = 1000,
+                   x0: bool = False, path: str = "auto", stream=None) -> MinresInfo:
+        """MINRES solve of KKT(tau, beta, n_t) x = rhs (device tensors [3, n_t, nz, ny, nx]);
+        x holds the initial guess when x0 is True.  Returns the iga_minres_info record."""
+        info = MinresInfo()
+        flags = PATHS[path] | (MINRES_X0 if x0 else 0)
+        _check(_lib.iga_kkt_minres(self._h, int(n_t), float(tau), float(beta), _tensor_ptr(rhs, "rhs"),
+                                   _tensor_ptr(x, "x"), float(rtol), int(maxit), flags, _stream_handle(stream),
+                                   ctypes.byref(info)))
+        return info
 
     # ------------------------------------------------------------------ host (end-to-end) applies
     def apply_host(self, x: np.ndarray, y_mass: Optional[np.ndarray], y_stiff: Optional[np.ndarray],

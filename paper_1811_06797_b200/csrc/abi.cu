@@ -26,6 +26,8 @@ iga_status cuda_error(cudaError_t e, const char* where) {
     return IGA_ECUDA;
 }
 
+void clear_error() { g_err.clear(); }
+
 // ------------------------------------------------------------------------------------
 // Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence, reading G1/G2).
 static void gauss_legendre(int m, double* x, double* w) {

@@ -94,6 +94,7 @@ namespace igalr {
 // ---- error plumbing (abi.cu)
 iga_status set_error(iga_status s, const std::string& msg);
 iga_status cuda_error(cudaError_t e, const char* where);
+void clear_error();
 
 // ---- factor assembly (factors.cu)
 struct DirQuad {
