@@ -126,27 +126,48 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
                          double* out, uint32_t flags, void* stream);
 
 /* ---------------------------------------------------------------- KKT solve (NEXT-1)
-   All-at-once solve of Eq. (KKTSystem) PAPER.md:313-319 for (y, u, lambda) by MINRES
-   (Paige & Saunders; the Krylov method the paper names for its reduced KKT systems,
-   PAPER.md:399-400), unpreconditioned, with iga_kkt_apply as the matvec.
-     rhs : DEVICE fp64 [3][n_t][Nz][Ny][Nx] (blocks y, u, lambda; e.g. [tau M yhat; 0; 0])
+   All-at-once solve of Eq. (KKTSystem) PAPER.md:313-319 for (y, u, lambda) by MINRES (Paige &
+   Saunders; the Krylov method the paper names for its reduced KKT systems),
+   with iga_kkt_apply as the matvec and an optional block-diagonal preconditioner.
+
+   Preconditioner (iga_kkt_prec_*): P = blkdiag(tau calMh, tau beta calMh, Sh), Sh the
+   Pearson-Stoll-Wathen "matching" Schur-complement approximation
+       Sh = (1/tau) (calKh + g calMh) calMh^{-1} (calKh + g calMh)',  g = tau / sqrt(beta),
+   with M, S replaced by mbar M0, sbar S0: the unit-weight Kronecker mass / Laplace-stiffness of
+   the op's spline spaces (factors of Eq. (massMatrix1D) with w = 1), scaled by the op's own
+   Rayleigh quotients on the smoothest mode.  All solves run in the fast-diagonalisation basis
+   of the univariate pencils (K0d, M0d); see DESIGN.md §11.  The preconditioner is tied to
+   (op extents, n_t, tau, beta) and must not outlive the op's device.
+     iga_kkt_prec_create : builds it (host eigen-decompositions + one op apply; synchronises).
+     iga_kkt_prec_apply  : out = P^{-1} in (DEVICE [3][n_t][Nz][Ny][Nx]; in != out).
+     iga_kkt_prec_info   : mbar, sbar and the univariate eigenvalues (HOST, m_x + m_y + m_z).
+   MINRES (iga_kkt_minres):
+     prec: NULL (P = I) or a preconditioner built for the same op, n_t, tau, beta.
+     rhs : DEVICE fp64 [3][n_t][Nz][Ny][Nx] (blocks y, u, lambda; e.g. [tau M yhat; 0; 0]).
      x   : DEVICE fp64, same layout.  On entry the initial guess if flags has IGA_MINRES_X0,
            otherwise ignored (x_0 = 0); on return the last MINRES iterate.
-     rtol: stop when |r_j| <= rtol |r_0| (|r_j| from the MINRES recurrence, |eta|);
-     maxit: iteration cap (0 => only r_0 is formed).
-     flags: IGA_PATH_* (passed to the matvec) | IGA_MINRES_X0.
-   Workspace (5 vectors) is stream-ordered scratch; the call synchronises `stream` once per
+     rtol: stop when |r_j|_{P^{-1}} <= rtol |r_0|_{P^{-1}} (|eta| of the recurrence);
+     maxit: iteration cap (0 => only r_0 is formed).   flags: IGA_PATH_* | IGA_MINRES_X0.
+   Workspace (7-8 vectors) is stream-ordered scratch; the call synchronises `stream` once per
    iteration (8-byte read of |eta|) and before returning.  Reductions are deterministic.
-   Errors: as iga_kkt_apply, plus IGA_EINVAL for rhs == x, maxit < 0, rtol < 0. */
+   Errors: as iga_kkt_apply, plus IGA_EINVAL for rhs == x, maxit < 0, rtol < 0, a
+   preconditioner built for other arguments. */
 #define IGA_MINRES_X0 0x100u
+typedef struct iga_kkt_prec iga_kkt_prec;
 typedef struct {
     int32_t iters;      /* MINRES iterations performed */
     int32_t converged;  /* 1 if |r| <= rtol |r_0| */
-    double relres;      /* |r_iters| / |r_0| (recurrence estimate) */
-    double res0;        /* |r_0| = |rhs - A x_0| */
+    double relres;      /* |r_iters| / |r_0| (recurrence estimate, P^{-1} norm) */
+    double res0;        /* |r_0| = |rhs - A x_0|_{P^{-1}} */
 } iga_minres_info;
-iga_status iga_kkt_minres(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* rhs, double* x,
-                          double rtol, int32_t maxit, uint32_t flags, void* stream, iga_minres_info* info);
+iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, double tau, double beta, uint32_t flags,
+                               void* stream, iga_kkt_prec** out);
+void iga_kkt_prec_destroy(iga_kkt_prec* prec);
+iga_status iga_kkt_prec_apply(const iga_kkt_prec* prec, const double* in, double* out, void* stream);
+iga_status iga_kkt_prec_info(const iga_kkt_prec* prec, double* mbar, double* sbar, double* lam);
+iga_status iga_kkt_minres(const iga_lr_op* op, const iga_kkt_prec* prec, int32_t n_t, double tau, double beta,
+                          const double* rhs, double* x, double rtol, int32_t maxit, uint32_t flags, void* stream,
+                          iga_minres_info* info);
 
 /* End-to-end variants with HOST buffers (pageable or pinned): copy in, apply, copy out,
    synchronise `stream`.  Device staging is stream-ordered scratch owned by the call. */

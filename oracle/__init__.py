@@ -334,53 +334,106 @@ def kkt_dense(M, S, n_t: int, tau: float, beta: float) -> np.ndarray:
     return np.block([[tau * calM, Z, calK.T], [Z, tau * beta * calM, -tau * calM], [calK, -tau * calM, Z]])
 
 
-def minres(matvec, b: np.ndarray, x0: Optional[np.ndarray] = None, maxit: int = 1000, rtol: float = 1e-8):
-    """MINRES for symmetric A (Paige & Saunders 1975), in the form of Elman, Silvester & Wathen,
-    Algorithm 2.4, with P = I, written out step by step:
+def minres(matvec, b: np.ndarray, x0: Optional[np.ndarray] = None, maxit: int = 1000, rtol: float = 1e-8,
+           precond=None):
+    """Preconditioned MINRES for symmetric A and SPD P (Paige & Saunders 1975), Elman, Silvester
+    & Wathen, Algorithm 2.4, written out step by step (P = I when precond is None):
 
-        q_0 = 0, r_0 = b - A x_0, gamma_1 = |r_0|, q_1 = r_0 / gamma_1, eta = gamma_1,
-        c_0 = c_1 = 1, s_0 = s_1 = 0, w_0 = w_1 = 0;  for j = 1, 2, ...
-          delta_j = q_j' A q_j
-          r = A q_j - delta_j q_j - gamma_j q_{j-1};  gamma_{j+1} = |r|;  q_{j+1} = r / gamma_{j+1}
+        v_0 = 0, w_0 = w_1 = 0, v_1 = b - A x_0, z_1 = P^{-1} v_1, gamma_1 = sqrt(z_1' v_1),
+        gamma_0 = 1, eta = gamma_1, s_0 = s_1 = 0, c_0 = c_1 = 1;  for j = 1, 2, ...
+          z_j = z_j / gamma_j;  delta_j = (A z_j)' z_j
+          v_{j+1} = A z_j - (delta_j / gamma_j) v_j - (gamma_j / gamma_{j-1}) v_{j-1}
+          z_{j+1} = P^{-1} v_{j+1};  gamma_{j+1} = sqrt(z_{j+1}' v_{j+1})
           a0 = c_j delta_j - c_{j-1} s_j gamma_j;  a1 = sqrt(a0^2 + gamma_{j+1}^2)
           a2 = s_j delta_j + c_{j-1} c_j gamma_j;  a3 = s_{j-1} gamma_j
           c_{j+1} = a0 / a1;  s_{j+1} = gamma_{j+1} / a1
-          w_{j+1} = (q_j - a3 w_{j-1} - a2 w_j) / a1;  x_j = x_{j-1} + c_{j+1} eta w_{j+1}
-          eta = -s_{j+1} eta
+          w_{j+1} = (z_j - a3 w_{j-1} - a2 w_j) / a1;  x_j = x_{j-1} + c_{j+1} eta w_{j+1}
+          eta = -s_{j+1} eta          (|eta| = |b - A x_j| in the P^{-1} norm)
 
-    Stops when |eta| <= rtol |r_0| or after maxit iterations.  Returns (x, iters, |eta|/|r_0|,
-    |r_0|).  Vectors are flat float64; `matvec` maps a flat vector to A times it."""
+    Stops when |eta| <= rtol gamma_1 or after maxit iterations.  Returns (x, iters, |eta| /
+    gamma_1, gamma_1).  Vectors are flat float64; matvec / precond map flat vectors."""
+    Pinv = (lambda v: v.copy()) if precond is None else precond
     b = np.asarray(b, dtype=np.float64).ravel()
     x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64).ravel()
-    r = b - matvec(x) if x0 is not None else b.copy()
-    gamma = float(np.sqrt(r @ r))
+    v = b - matvec(x) if x0 is not None else b.copy()
+    z = Pinv(v)
+    gamma = float(np.sqrt(max(z @ v, 0.0)))
+    gamma_prev = 1.0
     res0 = gamma
-    q_prev = np.zeros_like(b)
-    q = r / gamma if gamma > 0 else np.zeros_like(b)
+    v_prev = np.zeros_like(b)
     w_prev = np.zeros_like(b)
     w = np.zeros_like(b)
     eta = gamma
     c_prev = c = 1.0
     s_prev = s = 0.0
+    z = z / gamma if gamma > 0 else z * 0.0
     it = 0
     while it < maxit and abs(eta) > rtol * res0:
-        Aq = matvec(q)
-        delta = float(Aq @ q)
-        r = Aq - delta * q - gamma * q_prev
-        gamma_next = float(np.sqrt(r @ r))
+        Az = matvec(z)
+        delta = float(Az @ z)
+        v_next = Az - (delta / gamma) * v - (gamma / gamma_prev) * v_prev
+        z_next = Pinv(v_next)
+        gamma_next = float(np.sqrt(max(z_next @ v_next, 0.0)))
         a0 = c * delta - c_prev * s * gamma
         a1 = float(np.sqrt(a0 * a0 + gamma_next * gamma_next))
         a2 = s * delta + c_prev * c * gamma
         a3 = s_prev * gamma
         c_next = a0 / a1 if a1 > 0 else 1.0
         s_next = gamma_next / a1 if a1 > 0 else 0.0
-        w_next = (q - a3 * w_prev - a2 * w) / a1 if a1 > 0 else np.zeros_like(b)
+        w_next = (z - a3 * w_prev - a2 * w) / a1 if a1 > 0 else np.zeros_like(b)
         x = x + (c_next * eta) * w_next
         eta = -s_next * eta
-        q_prev, q = q, (r / gamma_next if gamma_next > 0 else np.zeros_like(b))
+        v_prev, v = v, v_next
+        z = z_next / gamma_next if gamma_next > 0 else z_next * 0.0
         w_prev, w = w, w_next
         c_prev, c = c, c_next
         s_prev, s = s, s_next
-        gamma = gamma_next
+        gamma_prev, gamma = gamma, gamma_next
         it += 1
     return x, it, (abs(eta) / res0 if res0 > 0 else 0.0), res0
+
+
+def kkt_prec_dense(P: "Problem", M, S, n_t: int, tau: float, beta: float, exact: bool = False):
+    """The block-diagonal KKT preconditioner of DESIGN.md §11 as a dense matrix (small sizes):
+
+        P = blkdiag(tau I (x) Mh,  tau beta I (x) Mh,  Sh),
+        Sh = (1/tau) G (I (x) Mh)^{-1} G',   G = I (x) (tau Sh0) + C (x) Mh + g I (x) Mh,
+        g = tau / sqrt(beta),  Mh = mbar M0,  Sh0 = sbar S0,
+
+    M0 = M0z (x) M0y (x) M0x and S0 = K0z(x)M0y(x)M0x + M0z(x)K0y(x)M0x + M0z(x)M0y(x)K0x from
+    the unit-weight univariate Grams (gram_1d with amp = 0, Eq. (massMatrix1D) PAPER.md:192-196;
+    patterns (0,0) and (1,1)), Dirichlet-sliced like the problem; mbar = v1' M v1 / v1' M0 v1 and
+    sbar = v1' S v1 / v1' S0 v1 for v1 = e1z (x) e1y (x) e1x, e1d the eigenvector of the smallest
+    eigenvalue of K0d v = lam M0d v (scipy.linalg.eigh).  exact=True uses M, S themselves
+    (Mh = M, Sh0 = S: the ideal matching preconditioner).  Returns (P, mbar, sbar, lam per dir)."""
+    import scipy.linalg as sla
+    M0d, K0d, e1, lams = [], [], [], []
+    for d in range(3):
+        kn, p = P.knots[d], P.p[d]
+        G0 = gram_1d(kn, p, P.nq, 0.0, 1.0, 0.0, 0, 0)
+        G1 = gram_1d(kn, p, P.nq, 0.0, 1.0, 0.0, 1, 1)
+        if P.dirichlet:
+            G0, G1 = G0[1:-1, 1:-1], G1[1:-1, 1:-1]
+        lam, V = sla.eigh(G1, G0)
+        M0d.append(G0)
+        K0d.append(G1)
+        e1.append(V[:, int(np.argmin(lam))])
+        lams.append(lam)
+    kron3 = lambda a, b, c: np.kron(c, np.kron(b, a))  # x fastest: (z) (x) (y) (x) (x)
+    M0 = kron3(M0d[0], M0d[1], M0d[2])
+    S0 = kron3(K0d[0], M0d[1], M0d[2]) + kron3(M0d[0], K0d[1], M0d[2]) + kron3(M0d[0], M0d[1], K0d[2])
+    v1 = kron3(e1[0][:, None], e1[1][:, None], e1[2][:, None]).ravel()
+    Md = M.toarray() if hasattr(M, "toarray") else np.asarray(M)
+    Sd = S.toarray() if hasattr(S, "toarray") else np.asarray(S)
+    mbar = (v1 @ Md @ v1) / (v1 @ M0 @ v1)
+    sbar = (v1 @ Sd @ v1) / (v1 @ S0 @ v1)
+    Mh, Sh0 = (Md, Sd) if exact else (mbar * M0, sbar * S0)
+    g = tau / np.sqrt(beta)
+    I = np.eye(n_t)
+    C = np.eye(n_t) - np.eye(n_t, k=-1)
+    G = np.kron(I, tau * Sh0) + np.kron(C, Mh) + g * np.kron(I, Mh)
+    calMh = np.kron(I, Mh)
+    Sh = (G @ np.linalg.solve(calMh, G.T)) / tau
+    Z = np.zeros_like(calMh)
+    Pm = np.block([[tau * calMh, Z, Z], [Z, tau * beta * calMh, Z], [Z, Z, Sh]])
+    return Pm, mbar, sbar, lams

@@ -35,7 +35,8 @@ STATUS_NAMES = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_ENOMEM", 3: "IGA_ECUDA", 4
 
 ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "iga_lr_apply", "iga_lr_apply2",
                "iga_kkt_apply", "iga_lr_apply_host", "iga_kkt_apply_host", "iga_lr_info", "iga_lr_export_factor",
-               "iga_last_error", "iga_version", "iga_kkt_minres"]
+               "iga_last_error", "iga_version", "iga_kkt_minres", "iga_kkt_prec_create", "iga_kkt_prec_destroy",
+               "iga_kkt_prec_apply", "iga_kkt_prec_info"]
 MINRES_X0 = 0x100
 
 
@@ -92,8 +93,14 @@ _lib.iga_lr_apply_host.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_dou
 _lib.iga_kkt_apply_host.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_uint32,
                                     _P]
 _lib.iga_lr_info.argtypes = [_P, ctypes.POINTER(_Info)]
-_lib.iga_kkt_minres.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_double,
+_lib.iga_kkt_minres.argtypes = [_P, _P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P, _P, ctypes.c_double,
                                 ctypes.c_int32, ctypes.c_uint32, _P, ctypes.POINTER(MinresInfo)]
+_lib.iga_kkt_prec_create.argtypes = [_P, ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_uint32, _P,
+                                     ctypes.POINTER(_P)]
+_lib.iga_kkt_prec_destroy.argtypes = [_P]
+_lib.iga_kkt_prec_destroy.restype = None
+_lib.iga_kkt_prec_apply.argtypes = [_P, _P, _P, _P]
+_lib.iga_kkt_prec_info.argtypes = [_P, _D, _D, _D]
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -257,15 +264,21 @@ class LowRankOperator:
                                   _tensor_ptr(out, "out"), PATHS[path], _stream_handle(stream)))
 
     def kkt_minres(self, rhs, x, n_t: int, tau: float, beta: float, rtol: float = 1e-8, maxit: int = 1000,
-                   x0: bool = False, path: str = "auto", stream=None) -> MinresInfo:
+                   x0: bool = False, prec: "Optional[KKTPreconditioner]" = None, path: str = "auto",
+                   stream=None) -> MinresInfo:
         """MINRES solve of KKT(tau, beta, n_t) x = rhs (device tensors [3, n_t, nz, ny, nx]);
-        x holds the initial guess when x0 is True.  Returns the iga_minres_info record."""
+        x holds the initial guess when x0 is True; prec: a KKTPreconditioner built for the same
+        (n_t, tau, beta) or None.  Returns the iga_minres_info record."""
         info = MinresInfo()
         flags = PATHS[path] | (MINRES_X0 if x0 else 0)
-        _check(_lib.iga_kkt_minres(self._h, int(n_t), float(tau), float(beta), _tensor_ptr(rhs, "rhs"),
-                                   _tensor_ptr(x, "x"), float(rtol), int(maxit), flags, _stream_handle(stream),
-                                   ctypes.byref(info)))
+        _check(_lib.iga_kkt_minres(self._h, prec._h if prec is not None else None, int(n_t), float(tau), float(beta),
+                                   _tensor_ptr(rhs, "rhs"), _tensor_ptr(x, "x"), float(rtol), int(maxit), flags,
+                                   _stream_handle(stream), ctypes.byref(info)))
         return info
+
+    def kkt_preconditioner(self, n_t: int, tau: float, beta: float, path: str = "auto",
+                           stream=None) -> "KKTPreconditioner":
+        return KKTPreconditioner(self, n_t, tau, beta, path, stream)
 
     # ------------------------------------------------------------------ host (end-to-end) applies
     def apply_host(self, x: np.ndarray, y_mass: Optional[np.ndarray], y_stiff: Optional[np.ndarray],
@@ -282,3 +295,40 @@ class LowRankOperator:
                        path: str = "auto", stream=None):
         _check(_lib.iga_kkt_apply_host(self._h, int(n_t), float(tau), float(beta), X.ctypes.data, out.ctypes.data,
                                        PATHS[path], _stream_handle(stream)))
+
+
+class KKTPreconditioner:
+    """Block-diagonal KKT preconditioner (iga_kkt_prec_*): blkdiag(tau Mh, tau beta Mh, Sh) with
+    Kronecker fast-diagonalisation solves (include/iga_lr.h)."""
+
+    def __init__(self, op: "LowRankOperator", n_t: int, tau: float, beta: float, path: str = "auto", stream=None):
+        h = _P()
+        _check(_lib.iga_kkt_prec_create(op._h, int(n_t), float(tau), float(beta), PATHS[path],
+                                        _stream_handle(stream), ctypes.byref(h)))
+        self._h = h.value
+        self._op = op  # keeps the op (and its device) alive
+        self.n_t, self.tau, self.beta = int(n_t), float(tau), float(beta)
+        self.dims = op.dims
+
+    def apply(self, r, out, stream=None):
+        """out = P^{-1} r for device tensors [3, n_t, nz, ny, nx]."""
+        _check(_lib.iga_kkt_prec_apply(self._h, _tensor_ptr(r, "r"), _tensor_ptr(out, "out"), _stream_handle(stream)))
+
+    def info(self):
+        mb, sb = ctypes.c_double(), ctypes.c_double()
+        lam = np.empty(sum(self.dims), dtype=np.float64)
+        _check(_lib.iga_kkt_prec_info(self._h, ctypes.byref(mb), ctypes.byref(sb),
+                                      lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        nx, ny, nz = self.dims
+        return mb.value, sb.value, (lam[:nx], lam[nx:nx + ny], lam[nx + ny:])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.iga_kkt_prec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -394,6 +394,7 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
         op->m[d] = dir ? op->n[d] - 2 : op->n[d];
     }
     for (int d = 0; d < 3; ++d) {
+        op->quad[d] = quad[d];
         iga_status s = assemble_dir(quad[d], tables[d], specs[d], dir, st, &op->F[d]);
         if (s) {
             iga_lr_destroy(op);

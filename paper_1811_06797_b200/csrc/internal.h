@@ -47,6 +47,15 @@ struct DirFactors {
     std::vector<int> table;    // dedup weight-table id per factor
 };
 
+// Univariate quadrature of one direction (A1): spans, Gauss nodes and weights.
+struct DirQuad {
+    int n, p, nq, ne;
+    std::vector<double> knots;
+    std::vector<int> span;       // [ne] knot-span index s of each nonempty span (first fn = s-p)
+    std::vector<double> node;    // [ne*nq]
+    std::vector<double> wgt;     // [ne*nq] Gauss weight * span length / 2
+};
+
 // Per-call output routing for kernels: groups of part g go to dst[g] with scale[g].
 struct OutMap {
     double* dst[2];   // output pointers for part 0 (mass) and 1 (stiffness); may alias
@@ -84,6 +93,7 @@ struct iga_lr_op {
     bool dirichlet;
     bool has_mass, has_stiff;
     igalr::DirFactors F[3];
+    igalr::DirQuad quad[3];   // (kept for derived operators: the KKT preconditioner)
     igalr::Plan plan[igalr::kNumPlans];
     double min_bytes = 0;
     int device = 0;
@@ -97,13 +107,6 @@ iga_status cuda_error(cudaError_t e, const char* where);
 void clear_error();
 
 // ---- factor assembly (factors.cu)
-struct DirQuad {
-    int n, p, nq, ne;
-    std::vector<double> knots;
-    std::vector<int> span;       // [ne] knot-span index s of each nonempty span (first fn = s-p)
-    std::vector<double> node;    // [ne*nq]
-    std::vector<double> wgt;     // [ne*nq] Gauss weight * span length / 2
-};
 struct FactorSpec {
     int table;    // weight table id (rows of `tables`)
     int a, b;     // derivative order on row / column function
@@ -126,6 +129,8 @@ iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const
                             int accumulate, int batch, cudaStream_t st);
 iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st);
+iga_status kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, double* tmp, cudaStream_t st);
+bool kkt_prec_matches(const iga_kkt_prec* P, const iga_lr_op* op, int n_t, double tau, double beta);
 iga_status kkt_combos(const double* in, double* abc, int n_t, int64_t N, double tau, double beta,
                       cudaStream_t st);
 

@@ -1,0 +1,366 @@
+// prec.cu — block-diagonal KKT preconditioner from Kronecker-structured solves (NEXT-1).
+//
+// For Eq. (KKTSystem),  A = [[tau calM, 0, calK'], [0, tau beta calM, -tau calM],
+// [calK, -tau calM, 0]]  with calM = I (x) M, calK = I (x) tau S + C (x) M, the
+// preconditioner is  P = blkdiag(tau calMh, tau beta calMh, Sh)  with the Schur-complement
+// approximation of Pearson, Stoll & Wathen ("matching"):
+//     Sh = (1/tau) (calKh + g calMh) calMh^{-1} (calKh + g calMh)',   g = tau / sqrt(beta),
+// where Mh = mbar M0, Sh0 = sbar S0 replace M and S by the unit-weight Kronecker operators
+//     M0 = M0z (x) M0y (x) M0x,   S0 = K0z(x)M0y(x)M0x + M0z(x)K0y(x)M0x + M0z(x)M0y(x)K0x
+// (univariate factors of Eq. (massMatrix1D) with w = 1 and the (1,1)-pattern stiffness factor,
+// PAPER.md:192-196, 217-220), scaled by Rayleigh quotients of the op's own M and S on the
+// smoothest mode.  Every solve is done in the fast-diagonalisation basis: per direction
+// K0d V = M0d V Lambda_d with V' M0d V = I, so with W = Vz (x) Vy (x) Vx
+//     M0^{-1} = W W',   (a M0 + b S0)^{-1} = W diag(1 / (a + b (lz + ly + lx))) W'.
+// calKh + g calMh is block lower bidiagonal in time (diagonal D = (1+g) Mh + tau Sh0, subdiagonal
+// -Mh), so Sh^{-1} = tau (calKh + g calMh)^{-T} calMh (calKh + g calMh)^{-1} becomes, in the
+// transformed variables, a forward and a backward first-order recurrence per spatial point:
+//     zc_k = (rc_k + mbar zc_{k-1}) / Delta,   vc_k = mbar (zc_k + vc_{k+1}) / Delta,   out = tau W vc
+// with Delta = (1+g) mbar + tau sbar (lz + ly + lx).  One application = two batched
+// three-mode dense transforms (W', W) plus the pointwise work.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+struct iga_kkt_prec {
+    int m[3];
+    int n_t;
+    double tau, beta, g, mbar, sbar;
+    double* dA[3];   // V_d  (row-major [m][m]: out index, in index)
+    double* dAt[3];  // V_d'
+    double* dlam[3];
+    int device;
+};
+
+namespace igalr {
+namespace {
+
+// ---- host dense linear algebra for the univariate generalised eigenproblems (m <= a few hundred)
+// Cholesky A = L L' (row-major, lower); false if not SPD
+bool cholesky(std::vector<double>& a, int n) {
+    for (int j = 0; j < n; ++j) {
+        double d = a[j * n + j];
+        for (int k = 0; k < j; ++k) d -= a[j * n + k] * a[j * n + k];
+        if (!(d > 0.0)) return false;
+        d = std::sqrt(d);
+        a[j * n + j] = d;
+        for (int i = j + 1; i < n; ++i) {
+            double s = a[i * n + j];
+            for (int k = 0; k < j; ++k) s -= a[i * n + k] * a[j * n + k];
+            a[i * n + j] = s / d;
+        }
+        for (int i = 0; i < j; ++i) a[i * n + j] = 0.0;
+    }
+    return true;
+}
+
+// cyclic Jacobi eigen-decomposition of symmetric C (row-major, destroyed): C = Q diag(lam) Q'
+void jacobi_eig(std::vector<double>& c, int n, std::vector<double>& q, std::vector<double>& lam) {
+    q.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) q[i * n + i] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) (i == j ? diag : off) += c[i * n + j] * c[i * n + j];
+        if (off <= 1e-32 * diag) break;
+        for (int p = 0; p < n - 1; ++p)
+            for (int r = p + 1; r < n; ++r) {
+                const double apr = c[p * n + r];
+                if (std::fabs(apr) < 1e-300) continue;
+                const double theta = (c[r * n + r] - c[p * n + p]) / (2.0 * apr);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < n; ++k) {  // columns p, r
+                    const double ckp = c[k * n + p], ckr = c[k * n + r];
+                    c[k * n + p] = cs * ckp - sn * ckr;
+                    c[k * n + r] = sn * ckp + cs * ckr;
+                }
+                for (int k = 0; k < n; ++k) {  // rows p, r
+                    const double cpk = c[p * n + k], crk = c[r * n + k];
+                    c[p * n + k] = cs * cpk - sn * crk;
+                    c[r * n + k] = sn * cpk + cs * crk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const double qkp = q[k * n + p], qkr = q[k * n + r];
+                    q[k * n + p] = cs * qkp - sn * qkr;
+                    q[k * n + r] = sn * qkp + cs * qkr;
+                }
+            }
+    }
+    lam.resize(n);
+    for (int i = 0; i < n; ++i) lam[i] = c[i * n + i];
+}
+
+// K v = lam M v with V' M V = I:  V = L^{-T} Q,  L^{-1} K L^{-T} = Q diag(lam) Q'
+bool gen_eig(std::vector<double> M, const std::vector<double>& K, int n, std::vector<double>& V,
+             std::vector<double>& lam) {
+    if (!cholesky(M, n)) return false;
+    const std::vector<double>& L = M;
+    std::vector<double> Y(K);  // Y = L^{-1} K  (forward substitution, column by column)
+    for (int col = 0; col < n; ++col)
+        for (int i = 0; i < n; ++i) {
+            double s = Y[i * n + col];
+            for (int k = 0; k < i; ++k) s -= L[i * n + k] * Y[k * n + col];
+            Y[i * n + col] = s / L[i * n + i];
+        }
+    std::vector<double> C((size_t)n * n);  // C = L^{-1} Y'  (= L^{-1} K L^{-T})
+    for (int col = 0; col < n; ++col)
+        for (int i = 0; i < n; ++i) {
+            double s = Y[col * n + i];
+            for (int k = 0; k < i; ++k) s -= L[i * n + k] * C[k * n + col];
+            C[i * n + col] = s / L[i * n + i];
+        }
+    for (int i = 0; i < n; ++i)  // symmetrise rounding
+        for (int j = i + 1; j < n; ++j) C[i * n + j] = C[j * n + i] = 0.5 * (C[i * n + j] + C[j * n + i]);
+    std::vector<double> Q;
+    jacobi_eig(C, n, Q, lam);
+    V.assign((size_t)n * n, 0.0);  // L' V = Q  (back substitution)
+    for (int col = 0; col < n; ++col)
+        for (int i = n - 1; i >= 0; --i) {
+            double s = Q[i * n + col];
+            for (int k = i + 1; k < n; ++k) s -= L[k * n + i] * V[k * n + col];
+            V[i * n + col] = s / L[i * n + i];
+        }
+    return true;
+}
+
+// ---- device kernels
+// out[o][i][c] = sum_j A[i][j] in[o][j][c]  (a dense mode product along the middle index)
+__global__ void k_mode(const double* __restrict__ A, const double* __restrict__ in, double* __restrict__ out,
+                       long long outer, int n, long long inner) {
+    const long long tot = outer * n * inner;
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < tot; g += (long long)gridDim.x * blockDim.x) {
+        const long long c = g % inner;
+        const long long oi = g / inner;
+        const int i = (int)(oi % n);
+        const long long o = oi / n;
+        const double* src = in + o * n * inner + c;
+        const double* a = A + (size_t)i * n;
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) acc = fma(__ldg(a + j), src[(long long)j * inner], acc);
+        out[g] = acc;
+    }
+}
+
+// pointwise part in the transformed basis: blocks y, u scaled; block lambda: the two recurrences
+__global__ void k_prec_point(double* __restrict__ t, int n_t, int mx, int my, int mz, const double* __restrict__ lx,
+                             const double* __restrict__ ly, const double* __restrict__ lz, double sy, double su,
+                             double dconst, double dlam, double mbar, double tau) {
+    const long long N = (long long)mx * my * mz;
+    const long long blk = (long long)n_t * N;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+        const int ix = (int)(p % mx), iy = (int)((p / mx) % my), iz = (int)(p / ((long long)mx * my));
+        const double delta = dconst + dlam * (lx[ix] + ly[iy] + lz[iz]);
+        const double inv = 1.0 / delta;
+        for (int k = 0; k < n_t; ++k) {
+            t[(long long)k * N + p] *= sy;
+            t[blk + (long long)k * N + p] *= su;
+        }
+        double* l = t + 2 * blk;
+        double z = 0.0;
+        for (int k = 0; k < n_t; ++k) {  // forward: zc_k = (rc_k + mbar zc_{k-1}) / Delta
+            z = (l[(long long)k * N + p] + mbar * z) * inv;
+            l[(long long)k * N + p] = z;
+        }
+        double v = 0.0;
+        for (int k = n_t - 1; k >= 0; --k) {  // backward: vc_k = mbar (zc_k + vc_{k+1}) / Delta
+            v = mbar * (l[(long long)k * N + p] + v) * inv;
+            l[(long long)k * N + p] = tau * v;
+        }
+    }
+}
+
+int grid_of(long long n) {
+    const long long nb = (n + 255) / 256;
+    return (int)(nb < 148 * 32 ? nb : 148 * 32);
+}
+
+// three mode products of W (trans = false) or W' (trans = true) on B vectors: in -> out (tmp used)
+void apply_W(const iga_kkt_prec* P, bool trans, long long B, const double* in, double* out, double* tmp,
+             cudaStream_t st) {
+    const long long mx = P->m[0], my = P->m[1], mz = P->m[2];
+    const double* const* A = trans ? P->dAt : P->dA;
+    const long long tot = B * mx * my * mz;
+    k_mode<<<grid_of(tot), 256, 0, st>>>(A[0], in, tmp, B * mz * my, (int)mx, 1);
+    k_mode<<<grid_of(tot), 256, 0, st>>>(A[1], tmp, out, B * mz, (int)my, mx);
+    k_mode<<<grid_of(tot), 256, 0, st>>>(A[2], out, tmp, B, (int)mz, my * mx);
+    cudaMemcpyAsync(out, tmp, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st);
+}
+
+}  // namespace
+
+iga_status kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, double* tmp, cudaStream_t st) {
+    const long long N = (long long)P->m[0] * P->m[1] * P->m[2];
+    const long long B = 3LL * P->n_t;
+    apply_W(P, true, B, in, out, tmp, st);  // out = W' in
+    k_prec_point<<<grid_of(N), 256, 0, st>>>(out, P->n_t, P->m[0], P->m[1], P->m[2], P->dlam[0], P->dlam[1],
+                                             P->dlam[2], 1.0 / (P->tau * P->mbar),
+                                             1.0 / (P->tau * P->beta * P->mbar), (1.0 + P->g) * P->mbar,
+                                             P->tau * P->sbar, P->mbar, P->tau);
+    apply_W(P, false, B, out, out, tmp, st);  // out = W out
+    cudaError_t e = cudaGetLastError();
+    if (e) return cuda_error(e, "kkt preconditioner");
+    return IGA_OK;
+}
+
+bool kkt_prec_matches(const iga_kkt_prec* P, const iga_lr_op* op, int n_t, double tau, double beta) {
+    return P->n_t == n_t && P->tau == tau && P->beta == beta && P->m[0] == op->m[0] && P->m[1] == op->m[1] &&
+           P->m[2] == op->m[2];
+}
+
+}  // namespace igalr
+
+using namespace igalr;
+
+extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, double tau, double beta, uint32_t flags,
+                                          void* stream, iga_kkt_prec** out) {
+    clear_error();
+    if (!op || !out) return set_error(IGA_EINVAL, "NULL op/out");
+    *out = nullptr;
+    if (!op->has_mass || !op->has_stiff) return set_error(IGA_ESTATE, "KKT needs mass and stiffness");
+    if (n_t < 1) return set_error(IGA_EINVAL, "n_t < 1");
+    if (!(tau > 0.0) || !std::isfinite(tau)) return set_error(IGA_EINVAL, "tau must be > 0");
+    if (!(beta > 0.0) || !std::isfinite(beta)) return set_error(IGA_EINVAL, "beta must be > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    iga_kkt_prec* P = new iga_kkt_prec();
+    memset(P, 0, sizeof *P);
+    P->n_t = n_t;
+    P->tau = tau;
+    P->beta = beta;
+    P->g = tau / std::sqrt(beta);
+    cudaGetDevice(&P->device);
+    std::vector<double> V[3], lam[3];
+    for (int d = 0; d < 3; ++d) {
+        const DirQuad& q = op->quad[d];
+        const int m = op->m[d];
+        P->m[d] = m;
+        // unit-weight univariate mass (0,0) and stiffness (1,1) factors
+        std::vector<std::vector<double>> tables(1, std::vector<double>(q.node.size(), 1.0));
+        std::vector<FactorSpec> specs = {{0, 0, 0}, {0, 1, 1}};
+        DirFactors F;
+        iga_status s = assemble_dir(q, tables, specs, op->dirichlet, st, &F);
+        if (s) {
+            iga_kkt_prec_destroy(P);
+            return s;
+        }
+        std::vector<double> band((size_t)2 * m * F.bw);
+        cudaError_t e = cudaMemcpy(band.data(), F.band, sizeof(double) * band.size(), cudaMemcpyDeviceToHost);
+        cudaFree(F.band);
+        if (e) {
+            iga_kkt_prec_destroy(P);
+            return cuda_error(e, "prec factors D2H");
+        }
+        std::vector<double> M0((size_t)m * m, 0.0), K0((size_t)m * m, 0.0);
+        const int p = F.p;
+        for (int i = 0; i < m; ++i)
+            for (int k = 0; k < F.bw; ++k) {
+                const int j = i - p + k;
+                if (j < 0 || j >= m) continue;
+                M0[(size_t)i * m + j] = band[(size_t)i * F.bw + k];
+                K0[(size_t)i * m + j] = band[((size_t)m + i) * F.bw + k];
+            }
+        if (!gen_eig(M0, K0, m, V[d], lam[d])) {
+            iga_kkt_prec_destroy(P);
+            return set_error(IGA_EINVAL, "unit-weight mass factor is not SPD");
+        }
+    }
+    // scalings: Rayleigh quotients of the op's M and S on the smoothest mode v1 = W e_(i0,j0,k0)
+    int i0[3];
+    for (int d = 0; d < 3; ++d) i0[d] = (int)(std::min_element(lam[d].begin(), lam[d].end()) - lam[d].begin());
+    const int mx = P->m[0], my = P->m[1], mz = P->m[2];
+    const size_t N = (size_t)mx * my * mz;
+    std::vector<double> v1(N), ym(N), ys(N);
+    for (int z = 0; z < mz; ++z)
+        for (int y = 0; y < my; ++y)
+            for (int x = 0; x < mx; ++x)
+                v1[((size_t)z * my + y) * mx + x] =
+                    V[2][(size_t)z * mz + i0[2]] * V[1][(size_t)y * my + i0[1]] * V[0][(size_t)x * mx + i0[0]];
+    double* dv = nullptr;
+    cudaError_t e = cudaMalloc(&dv, sizeof(double) * 3 * N);
+    if (!e) e = cudaMemcpy(dv, v1.data(), sizeof(double) * N, cudaMemcpyHostToDevice);
+    iga_status s = IGA_OK;
+    if (e) s = cuda_error(e, "prec scaling");
+    if (!s) s = iga_lr_apply(op, dv, dv + N, dv + 2 * N, 1.0, 1.0, 1, flags, stream);
+    if (!s) {
+        e = cudaStreamSynchronize(st);
+        if (!e) e = cudaMemcpy(ym.data(), dv + N, sizeof(double) * N, cudaMemcpyDeviceToHost);
+        if (!e) e = cudaMemcpy(ys.data(), dv + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost);
+        if (e) s = cuda_error(e, "prec scaling");
+    }
+    cudaFree(dv);
+    if (s) {
+        iga_kkt_prec_destroy(P);
+        return s;
+    }
+    double vm = 0.0, vs = 0.0;
+    for (size_t i = 0; i < N; ++i) {
+        vm += v1[i] * ym[i];
+        vs += v1[i] * ys[i];
+    }
+    P->mbar = vm;  // (v1' M0 v1 = 1)
+    P->sbar = vs / (lam[0][i0[0]] + lam[1][i0[1]] + lam[2][i0[2]]);
+    if (!(P->mbar > 0.0) || !(P->sbar > 0.0)) {
+        iga_kkt_prec_destroy(P);
+        return set_error(IGA_EINVAL, "preconditioner scalings are not positive");
+    }
+    for (int d = 0; d < 3; ++d) {
+        const int m = P->m[d];
+        std::vector<double> At((size_t)m * m);
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) At[(size_t)i * m + j] = V[d][(size_t)j * m + i];
+        e = cudaMalloc(&P->dA[d], sizeof(double) * m * m);
+        if (!e) e = cudaMalloc(&P->dAt[d], sizeof(double) * m * m);
+        if (!e) e = cudaMalloc(&P->dlam[d], sizeof(double) * m);
+        if (!e) e = cudaMemcpy(P->dA[d], V[d].data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
+        if (!e) e = cudaMemcpy(P->dAt[d], At.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
+        if (!e) e = cudaMemcpy(P->dlam[d], lam[d].data(), sizeof(double) * m, cudaMemcpyHostToDevice);
+        if (e) {
+            iga_kkt_prec_destroy(P);
+            return cuda_error(e, "prec upload");
+        }
+    }
+    *out = P;
+    return IGA_OK;
+}
+
+extern "C" void iga_kkt_prec_destroy(iga_kkt_prec* P) {
+    if (!P) return;
+    for (int d = 0; d < 3; ++d) {
+        if (P->dA[d]) cudaFree(P->dA[d]);
+        if (P->dAt[d]) cudaFree(P->dAt[d]);
+        if (P->dlam[d]) cudaFree(P->dlam[d]);
+    }
+    delete P;
+}
+
+extern "C" iga_status iga_kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, void* stream) {
+    clear_error();
+    if (!P || !in || !out) return set_error(IGA_EINVAL, "NULL argument");
+    if (in == out) return set_error(IGA_EINVAL, "in and out alias");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t tot = (size_t)3 * P->n_t * P->m[0] * P->m[1] * P->m[2];
+    double* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, sizeof(double) * tot, st);
+    if (e) return cuda_error(e, "cudaMallocAsync(prec)");
+    iga_status s = kkt_prec_apply(P, in, out, tmp, st);
+    cudaFreeAsync(tmp, st);
+    return s;
+}
+
+extern "C" iga_status iga_kkt_prec_info(const iga_kkt_prec* P, double* mbar, double* sbar, double* lam_out) {
+    clear_error();
+    if (!P) return set_error(IGA_EINVAL, "NULL prec");
+    if (mbar) *mbar = P->mbar;
+    if (sbar) *sbar = P->sbar;
+    if (lam_out) {
+        size_t off = 0;
+        for (int d = 0; d < 3; ++d) {
+            cudaError_t e = cudaMemcpy(lam_out + off, P->dlam[d], sizeof(double) * P->m[d], cudaMemcpyDeviceToHost);
+            if (e) return cuda_error(e, "prec info");
+            off += P->m[d];
+        }
+    }
+    return IGA_OK;
+}

@@ -115,3 +115,58 @@ def test_control_norm_decreases_with_beta():
         track.append(sum((X[0, k] - yhat[k]) @ oracle.spmv(M, X[0, k] - yhat[k]) for k in range(cfg.n_t)))
     assert unorm[0] > unorm[1] > unorm[2] > 0
     assert track[0] < track[1] < track[2]
+
+
+# ----------------------------------------------------------------------------- preconditioner
+def test_matching_schur_bounds():
+    # Pearson-Stoll-Wathen: with the exact M, S, the matching approximation Sh of the Schur
+    # complement S = (1/tau) K M^-1 K' + (tau/beta) M has eig(Sh^-1 S) in [1/2, 1]
+    cfg, M, S, beta = small_kkt(n=6, n_t=3, beta=1e-3)
+    P = oracle.problem_from_config(cfg, synth.draw_weights(cfg))
+    Pm, _, _, _ = oracle.kkt_prec_dense(P, M, S, cfg.n_t, cfg.tau, beta, exact=True)
+    N = M.shape[0]
+    nt, tau = cfg.n_t, cfg.tau
+    Md, Sd = M.toarray(), S.toarray()
+    I = np.eye(nt)
+    C = np.eye(nt) - np.eye(nt, k=-1)
+    K = np.kron(I, tau * Sd) + np.kron(C, Md)
+    calM = np.kron(I, Md)
+    Schur = K @ np.linalg.solve(calM, K.T) / tau + (tau / beta) * calM
+    Sh = Pm[2 * nt * N:, 2 * nt * N:]
+    ev = np.linalg.eigvals(np.linalg.solve(Sh, Schur)).real
+    assert ev.min() >= 0.5 - 1e-8 and ev.max() <= 1.0 + 1e-8
+
+
+def test_kronecker_preconditioner_spd_and_effective():
+    cfg, M, S, beta = small_kkt(n=7, n_t=3, beta=1e-4)
+    P = oracle.problem_from_config(cfg, synth.draw_weights(cfg))
+    Pm, mbar, sbar, lams = oracle.kkt_prec_dense(P, M, S, cfg.n_t, cfg.tau, beta)
+    assert np.allclose(Pm, Pm.T, rtol=0, atol=1e-14 * np.abs(Pm).max())
+    np.linalg.cholesky(Pm)  # SPD
+    assert mbar > 0 and sbar > 0 and all(l.min() > 0 for l in lams)
+    A = oracle.kkt_dense(M, S, cfg.n_t, cfg.tau, beta)
+    ev = np.abs(np.linalg.eigvals(np.linalg.solve(Pm, A)).real)
+    assert ev.max() / ev.min() < 50  # vs cond(A) ~ 1e10 unpreconditioned
+    b, _ = rhs_tracking(M, cfg.n_t, cfg.tau)
+    xs = np.linalg.solve(A, b)
+    x, it, relres, _ = oracle.minres(lambda v: A @ v, b, maxit=500, rtol=1e-10,
+                                     precond=lambda v: np.linalg.solve(Pm, v))
+    assert relres <= 1e-10 and it < 200
+    assert np.linalg.norm(x - xs) <= 1e-7 * np.linalg.norm(xs)
+
+
+def test_preconditioned_minres_first_iterate():
+    # x_1 minimises |b - A x|_{P^-1} over span{P^-1 b}:  x_1 = t P^-1 b,
+    # t = (b' P^-1 A P^-1 b) / (A P^-1 b)' P^-1 (A P^-1 b)
+    cfg, M, S, beta = small_kkt(n=6, n_t=2, beta=1e-2)
+    P = oracle.problem_from_config(cfg, synth.draw_weights(cfg))
+    Pm, _, _, _ = oracle.kkt_prec_dense(P, M, S, cfg.n_t, cfg.tau, beta)
+    A = oracle.kkt_dense(M, S, cfg.n_t, cfg.tau, beta)
+    b = np.random.default_rng(4).standard_normal(A.shape[0])
+    Pinv = lambda v: np.linalg.solve(Pm, v)
+    x1, it, _, _ = oracle.minres(lambda v: A @ v, b, maxit=1, rtol=0.0, precond=Pinv)
+    z = Pinv(b)
+    Az = A @ z
+    t = (b @ Pinv(Az)) / (Az @ Pinv(Az))
+    assert it == 1
+    assert np.linalg.norm(x1 - t * z) <= 1e-12 * np.linalg.norm(t * z)
