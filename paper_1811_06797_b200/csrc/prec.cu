@@ -126,6 +126,11 @@ bool gen_eig(std::vector<double> M, const std::vector<double>& K, int n, std::ve
     return true;
 }
 
+int grid_of(long long n) {
+    const long long nb = (n + 255) / 256;
+    return (int)(nb < 148 * 32 ? nb : 148 * 32);
+}
+
 // ---- device kernels
 // out[o][i][c] = sum_j A[i][j] in[o][j][c]  (a dense mode product along the middle index)
 __global__ void k_mode(const double* __restrict__ A, const double* __restrict__ in, double* __restrict__ out,
@@ -141,6 +146,121 @@ __global__ void k_mode(const double* __restrict__ A, const double* __restrict__ 
         double acc = 0.0;
         for (int j = 0; j < n; ++j) acc = fma(__ldg(a + j), src[(long long)j * inner], acc);
         out[g] = acc;
+    }
+}
+
+// Slab form of the same product for n <= 64: one CTA per (o, 64-column chunk), A and the input
+// slab staged in shared memory; warp w owns rows i = w, w+8, ..., each lane two columns.
+constexpr int kSlabC = 64;
+constexpr int kSlabRows = 8;  // rows per warp (n <= 64)
+__global__ void __launch_bounds__(256) k_mode_slab(const double* __restrict__ A, const double* __restrict__ in,
+                                                   double* __restrict__ out, long long outer, int n, long long inner) {
+    extern __shared__ double sm[];
+    double* As = sm;                      // [n][n+1]
+    double* Is = sm + n * (n + 1);        // [n][kSlabC]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) As[(t / n) * (n + 1) + t % n] = A[t];
+    const long long nchunk = (inner + kSlabC - 1) / kSlabC;
+    for (long long blk = blockIdx.x; blk < outer * nchunk; blk += gridDim.x) {
+        const long long o = blk / nchunk;
+        const long long c0 = (blk - o * nchunk) * kSlabC;
+        const int cw = (int)min((long long)kSlabC, inner - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < n * kSlabC; t += blockDim.x) {
+            const int j = t / kSlabC, cc = t % kSlabC;
+            Is[t] = cc < cw ? in[(o * n + j) * inner + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+        double acc[kSlabRows][2];
+#pragma unroll
+        for (int r = 0; r < kSlabRows; ++r) acc[r][0] = acc[r][1] = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double x0 = Is[j * kSlabC + lane], x1 = Is[j * kSlabC + lane + 32];
+#pragma unroll
+            for (int r = 0; r < kSlabRows; ++r) {
+                const int i = warp + 8 * r;
+                const double a = i < n ? As[i * (n + 1) + j] : 0.0;
+                acc[r][0] = fma(a, x0, acc[r][0]);
+                acc[r][1] = fma(a, x1, acc[r][1]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kSlabRows; ++r) {
+            const int i = warp + 8 * r;
+            if (i >= n) continue;
+            double* dst = out + (o * n + i) * inner + c0;
+            if (lane < cw) dst[lane] = acc[r][0];
+            if (lane + 32 < cw) dst[lane + 32] = acc[r][1];
+        }
+    }
+}
+
+// Contiguous-line form (inner = 1, n <= 64): out[o][i] = sum_j A[i][j] in[o][j]; one CTA per 64
+// lines, staged transposed (columns = lines) and written back through shared memory.
+__global__ void __launch_bounds__(256) k_mode_lines(const double* __restrict__ A, const double* __restrict__ in,
+                                                    double* __restrict__ out, long long outer, int n) {
+    extern __shared__ double sm[];
+    double* As = sm;                      // [n][n+1]
+    double* Is = sm + n * (n + 1);        // [n][kSlabC]  (Is[j][line])
+    double* Os = Is + n * kSlabC;         // [kSlabC][n+1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) As[(t / n) * (n + 1) + t % n] = A[t];
+    const long long nblk = (outer + kSlabC - 1) / kSlabC;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long o0 = blk * kSlabC;
+        const int cw = (int)min((long long)kSlabC, outer - o0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < kSlabC * n; t += blockDim.x) {  // contiguous global reads
+            const int ll = t / n, j = t % n;
+            Is[j * kSlabC + ll] = ll < cw ? in[(o0 + ll) * n + j] : 0.0;
+        }
+        __syncthreads();
+        double acc[kSlabRows][2];
+#pragma unroll
+        for (int r = 0; r < kSlabRows; ++r) acc[r][0] = acc[r][1] = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double x0 = Is[j * kSlabC + lane], x1 = Is[j * kSlabC + lane + 32];
+#pragma unroll
+            for (int r = 0; r < kSlabRows; ++r) {
+                const int i = warp + 8 * r;
+                const double a = i < n ? As[i * (n + 1) + j] : 0.0;
+                acc[r][0] = fma(a, x0, acc[r][0]);
+                acc[r][1] = fma(a, x1, acc[r][1]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kSlabRows; ++r) {
+            const int i = warp + 8 * r;
+            if (i >= n) continue;
+            Os[lane * (n + 1) + i] = acc[r][0];
+            Os[(lane + 32) * (n + 1) + i] = acc[r][1];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < cw * n; t += blockDim.x) {  // contiguous global writes
+            const int ll = t / n, i = t % n;
+            out[(o0 + ll) * n + i] = Os[ll * (n + 1) + i];
+        }
+    }
+}
+
+// out = A x_d in along the middle index of [outer][n][inner]
+void mode_product(const double* A, const double* in, double* out, long long outer, int n, long long inner,
+                  cudaStream_t st) {
+    const long long tot = outer * n * inner;
+    if (n > 8 * kSlabRows) {
+        k_mode<<<grid_of(tot), 256, 0, st>>>(A, in, out, outer, n, inner);
+        return;
+    }
+    if (inner == 1) {
+        const size_t sm = sizeof(double) * ((size_t)n * (n + 1) + (size_t)n * kSlabC + (size_t)kSlabC * (n + 1));
+        const long long nb = (outer + kSlabC - 1) / kSlabC;
+        cudaFuncSetAttribute(k_mode_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_mode_lines<<<(int)std::min(nb, 148LL * 8), 256, sm, st>>>(A, in, out, outer, n);
+    } else {
+        const size_t sm = sizeof(double) * ((size_t)n * (n + 1) + (size_t)n * kSlabC);
+        const long long nb = outer * ((inner + kSlabC - 1) / kSlabC);
+        cudaFuncSetAttribute(k_mode_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_mode_slab<<<(int)std::min(nb, 148LL * 8), 256, sm, st>>>(A, in, out, outer, n, inner);
     }
 }
 
@@ -172,20 +292,15 @@ __global__ void k_prec_point(double* __restrict__ t, int n_t, int mx, int my, in
     }
 }
 
-int grid_of(long long n) {
-    const long long nb = (n + 255) / 256;
-    return (int)(nb < 148 * 32 ? nb : 148 * 32);
-}
-
 // three mode products of W (trans = false) or W' (trans = true) on B vectors: in -> out (tmp used)
 void apply_W(const iga_kkt_prec* P, bool trans, long long B, const double* in, double* out, double* tmp,
              cudaStream_t st) {
     const long long mx = P->m[0], my = P->m[1], mz = P->m[2];
     const double* const* A = trans ? P->dAt : P->dA;
     const long long tot = B * mx * my * mz;
-    k_mode<<<grid_of(tot), 256, 0, st>>>(A[0], in, tmp, B * mz * my, (int)mx, 1);
-    k_mode<<<grid_of(tot), 256, 0, st>>>(A[1], tmp, out, B * mz, (int)my, mx);
-    k_mode<<<grid_of(tot), 256, 0, st>>>(A[2], out, tmp, B, (int)mz, my * mx);
+    mode_product(A[0], in, tmp, B * mz * my, (int)mx, 1, st);
+    mode_product(A[1], tmp, out, B * mz, (int)my, mx, st);
+    mode_product(A[2], out, tmp, B, (int)mz, my * mx, st);
     cudaMemcpyAsync(out, tmp, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st);
 }
 
