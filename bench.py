@@ -277,6 +277,38 @@ def cpu_oracle_rate(cfgname: str, seconds: float = 12.0):
             "sample": "%d random output rows (mass+stiffness) of %s, %.1f s" % (done, cfgname, el)}
 
 
+def time_kkt_solve(rtol: float = 1e-8):
+    """NEXT-1: all-at-once c4 KKT solve (preconditioned MINRES, iga_kkt_minres) for a tracking
+    right-hand side [tau M yhat; 0; 0]; wall time of the call (it synchronises per iteration)."""
+    import torch
+    import synth
+    from paper_1811_06797_b200 import workloads
+    cfg = synth.CONFIGS["c4"]
+    op = workloads.build_operator(cfg, synth.draw_weights(cfg))
+    m = cfg.n - 2
+    g = torch.Generator(device="cuda").manual_seed(7)
+    yhat = torch.randn((cfg.n_t, m, m, m), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.zeros((3, cfg.n_t, m, m, m), dtype=torch.float64, device="cuda")
+    ym = torch.empty_like(yhat)
+    op.apply(yhat, ym, None)
+    b[0] = cfg.tau * ym
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prec = op.kkt_preconditioner(cfg.n_t, cfg.tau, cfg.beta)
+    t1 = time.perf_counter()
+    x = torch.empty_like(b)
+    info = op.kkt_minres(b, x, cfg.n_t, cfg.tau, cfg.beta, rtol=rtol, maxit=3000, prec=prec)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    ax = torch.empty_like(b)
+    op.kkt_apply(x, ax, cfg.n_t, cfg.tau, cfg.beta)
+    rel2 = float(torch.linalg.vector_norm(b - ax) / torch.linalg.vector_norm(b))
+    unk = 3 * cfg.n_t * m ** 3
+    return {"workload": "c4_kkt_solve_pminres", "unknowns": unk, "rtol_Pinv_norm": rtol, "iters": info.iters,
+            "converged": bool(info.converged), "solve_s": t2 - t1, "ms_per_iter": 1e3 * (t2 - t1) / max(info.iters, 1),
+            "prec_setup_s": t1 - t0, "rel_residual_2norm": rel2}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -366,6 +398,10 @@ def main():
                 torch.cuda.empty_cache()
             except Exception as e:  # report, never hide
                 extra[other] = {"error": repr(e)}
+        try:
+            extra["c4_solve"] = time_kkt_solve()
+        except Exception as e:  # report, never hide
+            extra["c4_solve"] = {"error": repr(e)}
         line["configs"] = extra
     if rank == 0 and ws == 1:
         line["cpu_baseline"] = cpu_oracle_rate(a.config, seconds=a.cpu_seconds)
