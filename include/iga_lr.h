@@ -170,7 +170,10 @@ iga_status iga_kkt_minres(const iga_lr_op* op, const iga_kkt_prec* prec, int32_t
                           iga_minres_info* info);
 
 /* End-to-end variants with HOST buffers (pageable or pinned): copy in, apply, copy out,
-   synchronise `stream`.  Device staging is stream-ordered scratch owned by the call. */
+   synchronise `stream`.  Device staging is stream-ordered scratch owned by the call.
+   iga_lr_apply_host pipelines the batch vector by vector (H2D, apply, D2H on three streams
+   ordered by events): with pinned buffers both copy directions overlap the kernels.  Its
+   result equals per-vector iga_lr_apply calls bit for bit (and a batched call to rounding). */
 iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host,
                              double* y_stiff_host, double alpha, double gamma, int32_t batch, uint32_t flags,
                              void* stream);

@@ -601,27 +601,68 @@ static iga_status host_roundtrip(size_t in_elems, size_t out_elems, int nout, co
     return IGA_OK;
 }
 
+// Host-buffer apply.  The batch is pipelined vector by vector over three streams: H2D copies
+// (own stream), applies (the caller's stream) and D2H copies (own stream), ordered by events, so
+// with pinned host buffers the PCIe transfers in both directions overlap each other and the
+// kernels.  Device buffers are stream-ordered scratch on the caller's stream.
 iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host, double* y_stiff_host,
                              double alpha, double gamma, int32_t batch, uint32_t flags, void* stream) {
     g_err.clear();
     if (!op || !x_host || batch < 1 || (!y_mass_host && !y_stiff_host)) return set_error(IGA_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t tot = (size_t)op->m[0] * op->m[1] * op->m[2] * batch;
+    const size_t N = (size_t)op->m[0] * op->m[1] * op->m[2];
+    const size_t tot = N * batch;
     double *d_in = nullptr, *d_out = nullptr;
     const bool same = y_mass_host && y_mass_host == y_stiff_host;
     int nout = same ? 1 : (y_mass_host ? 1 : 0) + (y_stiff_host ? 1 : 0);
-    iga_status s = host_roundtrip(tot, tot, nout, x_host, nullptr, st, &d_in, &d_out);
+    cudaError_t e = cudaMallocAsync(&d_in, sizeof(double) * tot, st);
+    if (!e) e = cudaMallocAsync(&d_out, sizeof(double) * tot * nout, st);
+    if (e) {
+        if (d_in) cudaFreeAsync(d_in, st);
+        return cuda_error(e, "cudaMallocAsync(host apply)");
+    }
     double* dm = y_mass_host ? d_out : nullptr;
     double* ds = y_stiff_host ? (same ? d_out : d_out + (y_mass_host ? tot : 0)) : nullptr;
-    if (!s) s = iga_lr_apply(op, d_in, dm, ds, alpha, gamma, batch, flags, stream);
-    cudaError_t e = cudaSuccess;
-    if (!s && y_mass_host) e = cudaMemcpyAsync(y_mass_host, dm, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
-    if (!s && !e && y_stiff_host && !same) e = cudaMemcpyAsync(y_stiff_host, ds, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
-    if (d_in) cudaFreeAsync(d_in, st);
-    if (d_out) cudaFreeAsync(d_out, st);
+    const int nchunk = batch;
+    cudaStream_t sh = nullptr, sd = nullptr;
+    std::vector<cudaEvent_t> ev(2 * nchunk + 2, nullptr);
+    iga_status s = IGA_OK;
+    e = cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking);
+    if (!e) e = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+    for (size_t k = 0; k < ev.size() && !e; ++k) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+    if (!e) e = cudaEventRecord(ev[0], st);  // buffers allocated
+    if (!e) e = cudaStreamWaitEvent(sh, ev[0], 0);
+    if (!e) e = cudaStreamWaitEvent(sd, ev[0], 0);
+    for (int c = 0; c < nchunk && !e && !s; ++c) {
+        const size_t off = (size_t)c * N;
+        cudaEvent_t ein = ev[2 + 2 * c], eout = ev[3 + 2 * c];
+        e = cudaMemcpyAsync(d_in + off, x_host + off, sizeof(double) * N, cudaMemcpyHostToDevice, sh);
+        if (!e) e = cudaEventRecord(ein, sh);
+        if (!e) e = cudaStreamWaitEvent(st, ein, 0);
+        if (e) break;
+        s = iga_lr_apply(op, d_in + off, dm ? dm + off : nullptr, ds ? ds + off : nullptr, alpha, gamma, 1, flags,
+                         stream);
+        if (s) break;
+        e = cudaEventRecord(eout, st);
+        if (!e) e = cudaStreamWaitEvent(sd, eout, 0);
+        if (!e && y_mass_host)
+            e = cudaMemcpyAsync(y_mass_host + off, dm + off, sizeof(double) * N, cudaMemcpyDeviceToHost, sd);
+        if (!e && y_stiff_host && !same)
+            e = cudaMemcpyAsync(y_stiff_host + off, ds + off, sizeof(double) * N, cudaMemcpyDeviceToHost, sd);
+    }
+    // the caller's stream waits for the last D2H before the buffers are released
+    cudaError_t e3 = cudaEventRecord(ev[1], sd);
+    if (!e3) e3 = cudaStreamWaitEvent(st, ev[1], 0);
+    cudaFreeAsync(d_in, st);
+    cudaFreeAsync(d_out, st);
     cudaError_t e2 = cudaStreamSynchronize(st);
+    if (sh) cudaStreamDestroy(sh);
+    if (sd) cudaStreamDestroy(sd);
+    for (cudaEvent_t x : ev)
+        if (x) cudaEventDestroy(x);
     if (s) return s;
-    if (e) return cuda_error(e, "D2H");
+    if (e) return cuda_error(e, "host apply pipeline");
+    if (e3) return cuda_error(e3, "host apply pipeline");
     if (e2) return cuda_error(e2, "stream sync");
     return IGA_OK;
 }

@@ -309,7 +309,19 @@ def test_host_entry_points_match_device(env):
     hm = np.zeros_like(x)
     hs = np.zeros_like(x)
     op.apply_host(x, hm, hs)
-    assert np.array_equal(hm, dm) and np.array_equal(hs, ds)
+    # the host entry point pipelines the batch vector by vector (one apply per vector), so it
+    # equals per-vector device applies bit for bit and the batched apply to rounding
+    for b in range(2):
+        m1, s1 = gpu_apply(env, op, x[b:b + 1])
+        assert np.array_equal(hm[b], m1[0]) and np.array_equal(hs[b], s1[0])
+    assert rel(hm, dm) <= 1e-14 and rel(hs, ds) <= 1e-14
+    # summed output (y_mass_host == y_stiff_host) and mass-only
+    hsum = np.zeros_like(x)
+    op.apply_host(x, hsum, hsum, alpha=2.0, gamma=0.5)
+    assert rel(hsum, 2.0 * dm + 0.5 * ds) <= 1e-14
+    hm2 = np.zeros_like(x)
+    op.apply_host(x, hm2, None)
+    assert np.array_equal(hm2, hm)
 
 
 # ----------------------------------------------------------------------------- KKT
