@@ -169,6 +169,31 @@ iga_status iga_kkt_minres(const iga_lr_op* op, const iga_kkt_prec* prec, int32_t
                           const double* rhs, double* x, double rtol, int32_t maxit, uint32_t flags, void* stream,
                           iga_minres_info* info);
 
+/* ---------------------------------------------------------------- low-rank weights (NEXT-2)
+   The step before the path: samples of a weight function (omega =
+   |det grad G| or an entry q_kl of Q) at the Greville points of an interpolation space S~ ->
+   the rank-R separable form iga_sep that iga_lr_assemble_factors consumes.
+     iga_greville: Greville abscissae (t_{i+1} + ... + t_{i+p}) / p of one direction (HOST, n).
+     iga_weight_lowrank:
+       target : the op's space (its quadrature nodes tabulate the factors).
+       tilde  : 3 iga_dir of S~ (x, y, z); degree p~ <= 15.
+       samples: HOST fp64 [n~z][n~y][n~x], the weight at the Greville points (x fastest).
+       eps    : relative Frobenius accuracy of the TT-SVD of the samples (Oseledets'
+                truncation eps |.|_F / sqrt(D-1) per unfolding); 0 => exact up to rounding.
+       max_terms: cap on R = R1 R2.
+       Steps: TT-SVD (slowest direction first) -> the univariate collocation solves of
+       Eq. (weightEquationSolve) PAPER.md:256-262 per factor vector -> the R1 R2 canonical
+       terms of Eq. (TTranks) PAPER.md:243-246 tabulated at the target's nodes.
+       Errors: IGA_EINVAL (bad spaces, non-finite samples, singular collocation).
+     iga_weight_lowrank_sep: a view (valid until _free) as iga_sep (coef = 1), the TT ranks
+       (R1, R2) and the relative TT truncation error of the samples. */
+typedef struct iga_lowrank_weight iga_lowrank_weight;
+iga_status iga_greville(const iga_dir* d, double* out);
+iga_status iga_weight_lowrank(const iga_space* target, const iga_dir* tilde, const double* samples, double eps,
+                              int32_t max_terms, iga_lowrank_weight** out);
+iga_status iga_weight_lowrank_sep(const iga_lowrank_weight* w, iga_sep* sep, int32_t* tt_ranks, double* tt_error);
+void iga_weight_lowrank_free(iga_lowrank_weight* w);
+
 /* End-to-end variants with HOST buffers (pageable or pinned): copy in, apply, copy out,
    synchronise `stream`.  Device staging is stream-ordered scratch owned by the call.
    iga_lr_apply_host pipelines the batch vector by vector (H2D, apply, D2H on three streams

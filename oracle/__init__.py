@@ -22,8 +22,11 @@ What it computes (each function cites the passage it follows):
                           CSR M, S with calM = I (x) M, calK = I (x) tau S + C (x) M
                           (PAPER.md:316-318), for small sizes (dense LU solves, pins).
 * ``minres``              MINRES (Paige & Saunders), the recurrence of Elman-Silvester-Wathen
-                          Algorithm 2.4 with P = I, step by step (the Krylov method of
-                          PAPER.md:399-400; NEXT-1 of SURVEY.md §8(f)).
+                          Algorithm 2.4, step by step (the Krylov method of PAPER.md:399-400;
+                          NEXT-1 of SURVEY.md §8(f)); ``kkt_prec_dense`` its block preconditioner.
+* ``greville``, ``tt_svd``, ``weight_lowrank``  NEXT-2: samples at Greville points -> TT-SVD ->
+                          univariate collocation solves -> canonical terms tabulated at nodes
+                          (PAPER.md:177-265).
 
 Parity pins: tests/test_oracle_pins.py (P1-P12 of SURVEY.md §8(c)).
 Every function here is pinned; none is "parity unpinned".
@@ -437,3 +440,62 @@ def kkt_prec_dense(P: "Problem", M, S, n_t: int, tau: float, beta: float, exact:
     Z = np.zeros_like(calMh)
     Pm = np.block([[tau * calMh, Z, Z], [Z, tau * beta * calMh, Z], [Z, Z, Sh]])
     return Pm, mbar, sbar, lams
+
+
+# ----------------------------------------------------------------------------- NEXT-2 (weights)
+def greville(knots, p: int) -> np.ndarray:
+    """Greville abscissae xi*_i = (t_{i+1} + ... + t_{i+p}) / p (the interpolation points)."""
+    t = np.asarray(knots, dtype=np.float64)
+    n = len(t) - p - 1
+    return np.array([t[i + 1:i + p + 1].sum() / p for i in range(n)])
+
+
+def collocation(knots, p: int, pts) -> np.ndarray:
+    """B[i, j] = beta_j(pts_i) from the full Cox-de Boor triangle (basis_all)."""
+    t = np.asarray(knots, dtype=np.float64)
+    n = len(t) - p - 1
+    return np.array([basis_all(t, p, float(x))[0][:n] for x in pts])
+
+
+def tt_svd(S: np.ndarray, eps: float):
+    """TT-SVD (Oseledets 2011) of a 3-way tensor S[z, y, x] (slowest first), truncating each
+    unfolding to the smallest rank whose discarded singular values have squared sum
+    <= (eps |S|_F / sqrt(2))^2.  Returns cores (G1 [nz, R1], G2 [R1, ny, R2], G3 [R2, nx])."""
+    nz, ny, nx = S.shape
+    d2 = (eps * np.linalg.norm(S)) ** 2 / 2.0
+
+    def rank(sv):
+        r = len(sv)
+        tail = 0.0
+        while r > 1 and tail + sv[r - 1] ** 2 <= d2:
+            tail += sv[r - 1] ** 2
+            r -= 1
+        return r
+
+    U, sv, Vt = np.linalg.svd(S.reshape(nz, ny * nx), full_matrices=False)
+    R1 = rank(sv)
+    G1 = U[:, :R1]
+    C = (sv[:R1, None] * Vt[:R1]).reshape(R1 * ny, nx)
+    U, sv, Vt = np.linalg.svd(C, full_matrices=False)
+    R2 = rank(sv)
+    G2 = U[:, :R2].reshape(R1, ny, R2)
+    G3 = sv[:R2, None] * Vt[:R2]
+    return G1, G2, G3
+
+
+def weight_lowrank(nodes, tilde_knots, tilde_p, samples: np.ndarray, eps: float):
+    """Eqs. (TTranks) PAPER.md:243-246 and (weightEquationSolve) PAPER.md:256-262: the TT
+    cores of the samples, each factor vector solved against the univariate collocation matrix
+    at the Greville points, the R1 R2 canonical terms evaluated at `nodes` (per direction x, y,
+    z).  Returns tabs [x, y, z], each [R, len(nodes_d)], and the TT ranks."""
+    G1, G2, G3 = tt_svd(np.asarray(samples, dtype=np.float64), eps)
+    R1, R2 = G1.shape[1], G3.shape[0]
+    B = [collocation(tilde_knots[d], tilde_p[d], greville(tilde_knots[d], tilde_p[d])) for d in range(3)]
+    E = [collocation(tilde_knots[d], tilde_p[d], nodes[d]) for d in range(3)]
+    tabs = [np.zeros((R1 * R2, len(nodes[d]))) for d in range(3)]
+    for r1 in range(R1):
+        for r2 in range(R2):
+            r = r1 * R2 + r2
+            for d, f in ((2, G1[:, r1]), (1, G2[r1, :, r2]), (0, G3[r2, :])):
+                tabs[d][r] = E[d] @ np.linalg.solve(B[d], f)
+    return tabs, (R1, R2)

@@ -36,7 +36,8 @@ STATUS_NAMES = {0: "IGA_OK", 1: "IGA_EINVAL", 2: "IGA_ENOMEM", 3: "IGA_ECUDA", 4
 ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "iga_lr_apply", "iga_lr_apply2",
                "iga_kkt_apply", "iga_lr_apply_host", "iga_kkt_apply_host", "iga_lr_info", "iga_lr_export_factor",
                "iga_last_error", "iga_version", "iga_kkt_minres", "iga_kkt_prec_create", "iga_kkt_prec_destroy",
-               "iga_kkt_prec_apply", "iga_kkt_prec_info"]
+               "iga_kkt_prec_apply", "iga_kkt_prec_info", "iga_greville", "iga_weight_lowrank",
+               "iga_weight_lowrank_sep", "iga_weight_lowrank_free"]
 MINRES_X0 = 0x100
 
 
@@ -101,6 +102,13 @@ _lib.iga_kkt_prec_destroy.argtypes = [_P]
 _lib.iga_kkt_prec_destroy.restype = None
 _lib.iga_kkt_prec_apply.argtypes = [_P, _P, _P, _P]
 _lib.iga_kkt_prec_info.argtypes = [_P, _D, _D, _D]
+_lib.iga_greville.argtypes = [ctypes.POINTER(_Dir), _D]
+_lib.iga_weight_lowrank.argtypes = [ctypes.POINTER(_Space), ctypes.POINTER(_Dir), _D, ctypes.c_double, ctypes.c_int32,
+                                    ctypes.POINTER(_P)]
+_lib.iga_weight_lowrank_sep.argtypes = [_P, ctypes.POINTER(_Sep), ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(ctypes.c_double)]
+_lib.iga_weight_lowrank_free.argtypes = [_P]
+_lib.iga_weight_lowrank_free.restype = None
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -162,6 +170,47 @@ def _tensor_ptr(t, name: str) -> int:
     if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
         raise ValueError("%s must be a contiguous float64 CUDA tensor" % name)
     return t.data_ptr()
+
+
+def greville(knots: np.ndarray, p: int) -> np.ndarray:
+    """Greville abscissae of one univariate space (iga_greville)."""
+    k = np.ascontiguousarray(knots, dtype=np.float64)
+    d = _Dir()
+    d.p, d.n, d.knots = int(p), int(len(k) - p - 1), _dptr(k)
+    out = np.zeros(d.n)
+    _check(_lib.iga_greville(ctypes.byref(d), _dptr(out)))
+    return out
+
+
+def weight_lowrank(target_knots: Sequence[np.ndarray], target_p: Sequence[int], tilde_knots: Sequence[np.ndarray],
+                   tilde_p: Sequence[int], samples: np.ndarray, eps: float = 1e-10, max_terms: int = 64,
+                   nq: int = 0):
+    """Rank-R separable weight from samples at the Greville points of S~ (iga_weight_lowrank,
+    NEXT-2).  samples: [n~z, n~y, n~x].  Returns (SepWeight tabulated at the target's
+    quadrature nodes, (R1, R2) TT ranks, relative TT truncation error of the samples)."""
+    sp, keep = _space(target_knots, target_p, nq)
+    tk = [np.ascontiguousarray(k, dtype=np.float64) for k in tilde_knots]
+    td = (_Dir * 3)()
+    for d in range(3):
+        td[d].p, td[d].n, td[d].knots = int(tilde_p[d]), int(len(tk[d]) - int(tilde_p[d]) - 1), _dptr(tk[d])
+    smp = np.ascontiguousarray(samples, dtype=np.float64)
+    if smp.shape != (td[2].n, td[1].n, td[0].n):
+        raise ValueError("samples must be [n~z, n~y, n~x]")
+    h = _P()
+    _check(_lib.iga_weight_lowrank(ctypes.byref(sp), td, _dptr(smp), float(eps), int(max_terms), ctypes.byref(h)))
+    try:
+        sep = _Sep()
+        ranks = (ctypes.c_int32 * 2)()
+        err = ctypes.c_double()
+        _check(_lib.iga_weight_lowrank_sep(h, ctypes.byref(sep), ranks, ctypes.byref(err)))
+        nodes = quad_nodes(target_knots, target_p, nq)
+        R = int(sep.R)
+        tabs = [np.ctypeslib.as_array(sep.tab[d], shape=(R * len(nodes[d]),)).reshape(R, len(nodes[d])).copy()
+                for d in range(3)]
+        coef = np.ctypeslib.as_array(sep.coef, shape=(R,)).copy()
+        return SepWeight(coef, tabs), (int(ranks[0]), int(ranks[1])), float(err.value)
+    finally:
+        _lib.iga_weight_lowrank_free(h)
 
 
 class SepWeight:
