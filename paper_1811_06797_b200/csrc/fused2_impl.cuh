@@ -1431,29 +1431,39 @@ struct CanonCfg {
     static constexpr int WPQ = 2;                // warps per TMEM lane quadrant
 };
 
-// tile shape: QX quadrants across x; pick the least padding waste (ties -> wider)
-static int pick_qx(int mx, int my, int P) {
-    const int LW = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
-    int best = 4;
-    double bw = 1e30;
-    for (int qx : {4, 2, 1}) {
-        const int tx = 32 * qx, ty = LW * 2 * (4 / qx);
+// Tile shape: QX quadrants across x and LW rows per warp.  Candidates: the degree's default LW
+// with QX in {4, 2, 1}, plus (p = 3) LW = 12 with QX = 2 for meshes whose extent 32 LW tiles
+// badly (e.g. 46 interior rows: 48-row tiles instead of 64).  Cost = padded area x the X stage's
+// y-halo recompute (the X stage is ~1/5 of a point's FP64 work).  Ties -> the first candidate.
+struct TileChoice {
+    int qx, lw;
+};
+static TileChoice pick_tile(int mx, int my, int P) {
+    const int LW0 = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
+    TileChoice cand[4] = {{4, LW0}, {2, LW0}, {1, LW0}, {2, 12}};
+    const int ncand = (P == 3) ? 4 : 3;
+    TileChoice best = cand[0];
+    double bc = 1e30;
+    for (int i = 0; i < ncand; ++i) {
+        const int tx = 32 * cand[i].qx, ty = cand[i].lw * 2 * (4 / cand[i].qx);
         const double waste = (double)((mx + tx - 1) / tx * tx) / mx * (double)((my + ty - 1) / ty * ty) / my;
-        if (waste < bw - 1e-9) {
-            bw = waste;
-            best = qx;
+        const double halo = (double)(cand[i].lw + 2 * P) / cand[i].lw;
+        const double cost = waste * (0.8 + 0.2 * halo);
+        if (cost < bc - 1e-9) {
+            bc = cost;
+            best = cand[i];
         }
     }
     const char* s = getenv("IGALR_QX");
-    if (s && (s[0] == '1' || s[0] == '2' || s[0] == '4')) best = s[0] - '0';
+    if (s && (s[0] == '1' || s[0] == '2' || s[0] == '4')) best = {s[0] - '0', LW0};
     return best;
 }
 
-template <class S, int P, int QX, bool YRES, bool TMA>
+template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW>
 cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st) {
     using namespace f2;
-    constexpr int LW = CanonCfg<P>::LW, WPQ = CanonCfg<P>::WPQ;
+    constexpr int WPQ = CanonCfg<P>::WPQ;
     constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
     Args2 a;
     memset(&a, 0, sizeof a);
@@ -1504,9 +1514,9 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     return e;
 }
 
-template <class S, int P, int QX>
+template <class S, int P, int QX, int LW = CanonCfg<P>::LW>
 bool yres_fits(int nrounds) {
-    return f2::smem_bytes_canon<S, P, CanonCfg<P>::LW, 2, QX, true>(nrounds) <= 227 * 1024;
+    return f2::smem_bytes_canon<S, P, LW, 2, QX, true>(nrounds) <= 227 * 1024;
 }
 
 template <class S>
@@ -1525,7 +1535,7 @@ size_t canon_smem(int p, int nrounds) {
     return m;
 }
 
-template <class S, int P, int QX>
+template <class S, int P, int QX, int LW = CanonCfg<P>::LW>
 cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st) {
     const char* s = getenv("IGALR_YRES");
@@ -1535,7 +1545,12 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     // bulk copies need 16-byte aligned coefficient rows: (factor * nx + x0) * BW even <=> nx even
     // the GSYNC path (TMA && YRES) also bulk-copies plane rows: 16-byte aligned input
     const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
-    const bool yres = !force_off && yres_fits<S, P, QX>(pl.canon_nrounds);
+    const bool yres = !force_off && yres_fits<S, P, QX, LW>(pl.canon_nrounds);
+    if constexpr (LW != CanonCfg<P>::LW) {
+        // alternative row count: instantiated for the GSYNC path only
+        if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st);
+        return launch_canon_q<S, P, QX>(op, pl, src, dst, scale, accumulate, batch, st);
+    }
     if (tma) {
         if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st);
         return launch_canon_t<S, P, QX, false, true>(op, pl, src, dst, scale, accumulate, batch, st);
@@ -1556,9 +1571,12 @@ cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const
 template <class S, int P>
 cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st) {
-    const int qx = pick_qx(op->m[0], op->m[1], P);
-    if (qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st);
-    if (qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st);
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
+    if constexpr (P == 3) {
+        if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st);
+    }
+    if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st);
     return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st);
 }
 #define IGALR_CAT2(a, b) a##b
