@@ -444,6 +444,10 @@ void iga_lr_destroy(iga_lr_op* op) {
         if (op->plan[k].d_canon) cudaFree(op->plan[k].d_canon);
         if (op->plan[k].d_ztab) cudaFree(op->plan[k].d_ztab);
     }
+    if (op->side) cudaStreamDestroy(op->side);
+    for (auto& c : op->fix_cache) {
+        if (c.d_tab) cudaFree(c.d_tab);
+    }
     delete op;
 }
 
@@ -472,13 +476,41 @@ static iga_status run_f2(const iga_lr_op* op, const double* xm, const double* xs
     iga_status s = IGA_OK;
     const char* gen = getenv("IGALR_F2_GENERIC");
     const bool canon_ok = !(gen && gen[0] == '1');
-    auto part_run = [&](int part, const double* x, double* d, double sc, int acc) {
+    auto part_run = [&](int part, const double* x, double* d, double sc, int acc, cudaStream_t ps) {
         const Plan& pl = op->plan[part ? kPlanF2Stiff : kPlanF2Mass];
-        if (canon_ok && pl.canon_ok) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, st);
-        return apply_fused2_part(op, pl, part, x, d, sc, acc, batch, st);
+        if (canon_ok && pl.canon_ok) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, ps);
+        return apply_fused2_part(op, pl, part, x, d, sc, acc, batch, ps);
     };
-    if (need_m) s = part_run(0, xm, dm, alpha, 0);
-    if (!s && need_s) s = part_run(1, xs, ds, gamma, (need_m && dm == ds) ? 1 : 0);
+    if (need_m && need_s && dm != ds && canon_small_grid(op, batch)) {
+        // small meshes: neither persistent grid fills the GPU, so the mass part runs on a side
+        // stream beside the stiffness part (fork/join with events; outputs do not alias)
+        cudaStream_t side = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(op->fix_mu);
+            if (!op->side && cudaStreamCreateWithFlags(&op->side, cudaStreamNonBlocking) != cudaSuccess)
+                op->side = nullptr;
+            side = op->side;
+        }
+        cudaEvent_t ef = nullptr, ej = nullptr;
+        if (side && cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) == cudaSuccess) {
+            cudaError_t e = cudaEventRecord(ef, st);
+            if (!e) e = cudaStreamWaitEvent(side, ef, 0);
+            if (e) return cuda_error(e, "fork");
+            s = part_run(0, xm, dm, alpha, 0, side);
+            const cudaError_t e2 = cudaEventRecord(ej, side);
+            if (!s) s = part_run(1, xs, ds, gamma, 0, st);
+            const cudaError_t e3 = cudaStreamWaitEvent(st, ej, 0);  // join (also on error)
+            cudaEventDestroy(ef);
+            cudaEventDestroy(ej);
+            if (!s && (e2 || e3)) return cuda_error(e2 ? e2 : e3, "join");
+            return s;
+        }
+        if (ef) cudaEventDestroy(ef);
+        if (ej) cudaEventDestroy(ej);
+    }
+    if (need_m) s = part_run(0, xm, dm, alpha, 0, st);
+    if (!s && need_s) s = part_run(1, xs, ds, gamma, (need_m && dm == ds) ? 1 : 0, st);
     return s;
 }
 

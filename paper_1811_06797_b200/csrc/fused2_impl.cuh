@@ -23,6 +23,8 @@
 
 #include <cuda.h>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -255,7 +257,7 @@ struct Geo {
 };
 
 // scratch slot of a partial output plane zo for a segment [za, zb) (see header comment)
-__device__ __forceinline__ int partial_slot(int zo, int za, int zb, int P) {
+__host__ __device__ __forceinline__ int partial_slot(int zo, int za, int zb, int P) {
     const int rel = zo - (za - P);
     if (rel < 2 * P) return rel;                  // head band
     return 2 * P + (zo - (zb - P));               // tail band
@@ -626,12 +628,16 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int quad = warp & 3, sub = warp >> 2;
-    const int cx = (quad % QX) * TXW + lane;                 // tile column of this thread
-    // GSYNC: the warps of one column group (same quad % QX: 32 columns) are the only readers of
+    // column group of this warp: the WPQ warps that share a TMEM lane quadrant (and so an SMSP:
+    // warp % 4) take different column groups, so a group barrier never holds both warps of one
+    // scheduler at once (the other keeps the FP64 pipe busy)
+    const int cg = (quad + sub) % QX;
+    const int cx = cg * TXW + lane;                          // tile column of this thread
+    // GSYNC: the warps of one column group (same cg: 32 columns) are the only readers of
     // the group's x-coefficients, so rounds are separated by a group barrier (named barrier
     // 1 + grp) and only the first round of a plane (new plane buffer) by a CTA barrier.
     constexpr bool GSYNC = gsync_path<P, TMA, YRES>();
-    const int grp = GSYNC ? quad % QX : 0;
+    const int grp = GSYNC ? cg : 0;
     constexpr int GTHREADS = GSYNC ? 32 * WPQ * (4 / QX) : NW * WPQ * 32;
     const bool gprod = GSYNC ? (warp == grp && lane == 0) : (threadIdx.x == 0);  // x-copy issuer
     const int row0 = ((quad / QX) * WPQ + sub) * LW;          // first tile output row of this warp
@@ -1077,63 +1083,28 @@ static __global__ void k_fixup(const Args2 a, int P, int L) {
     }
 }
 
-// k_fixup for the canonical kernels (tile TY x TX, TX a multiple of 4): the same contributor
-// search and summation order, with each thread summing 4 consecutive points per step and all
-// partial loads of a thread issued before its stores (the plane-sized loop is latency-bound).
-static __global__ void __launch_bounds__(256) k_fixup4(const Args2 a, int P) {
-    __shared__ int s_valid, s_n, s_b, s_zo, s_txi, s_tyi;
-    __shared__ long long s_off[8];
-    const int kb = 1 + blockIdx.x / (2 * P);
-    const int s = blockIdx.x % (2 * P);
+// Fixup of the canonical kernels, driven by a host-built table (fixup_table): one CTA per partial
+// output plane of a tile, summing its contributors' scratch planes in CTA order (deterministic;
+// no atomics, no on-device contributor search).  Each thread sums 4 consecutive points per step,
+// with all partial loads of a thread issued before its stores.
+struct FixEnt {
+    int b, zo, txi, tyi;
+    int n, pad;
+    long long off[2 * 4 + 1];  // scratch offsets of the contributors (<= 2P+1), CTA order
+};
+static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const FixEnt* __restrict__ tab) {
+    const FixEnt& E = tab[blockIdx.x];
     const int TY = a.tyt, TX = a.txt;
-    if (threadIdx.x == 0) {
-        s_valid = 0;
-        s_n = 0;
-        const long long ub = unit_begin(kb, a.units, a.nctas);
-        const long long tile = ub / a.mz;
-        const int zbnd = (int)(ub - tile * a.mz);
-        const int zo = zbnd - P + s;
-        if (zbnd != 0 && zo >= 0 && zo < a.mz) {
-            long long tt = tile;
-            s_txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
-            s_tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
-            s_b = (int)tt;
-            s_zo = zo;
-            const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
-            const long long ulo = tile * a.mz + lo, uhi = tile * a.mz + hi;
-            long long k0 = kb - 1, k1 = kb;
-            while (k0 > 0 && unit_begin(k0, a.units, a.nctas) > ulo) --k0;
-            while (k1 + 1 < a.nctas && unit_begin(k1 + 1, a.units, a.nctas) <= uhi) ++k1;
-            for (long long k = k0; k <= k1 && s_n < 8; ++k) {
-                const long long cu0 = unit_begin(k, a.units, a.nctas), cu1 = unit_begin(k + 1, a.units, a.nctas);
-                int seg = 0;
-                for (long long u = cu0; u < cu1; ++seg) {
-                    const long long t2 = u / a.mz;
-                    const int sa = (int)(u - t2 * a.mz);
-                    const int sb = (int)min((long long)a.mz, (long long)sa + (cu1 - u));
-                    if (t2 == tile) {
-                        const int slot = partial_slot(zo, sa, sb, P);
-                        s_off[s_n++] = (((long long)k * NSEG + seg) * 4 * P + slot) * (long long)TY * TX;
-                        break;
-                    }
-                    u += sb - sa;
-                }
-            }
-            s_valid = 1;
-        }
-    }
-    __syncthreads();
-    if (!s_valid) return;
     const long long plane = (long long)a.mx * a.my;
-    const long long obase = (long long)s_b * a.mz * plane + (long long)s_zo * plane;
-    const int n = s_n;
+    const long long obase = (long long)E.b * a.mz * plane + (long long)E.zo * plane;
+    const int n = E.n;
     const int nq = TY * TX / 4;
     for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * blockDim.x) {
         double4 acc[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) acc[t] = make_double4(0.0, 0.0, 0.0, 0.0);
         for (int c = 0; c < n; ++c) {
-            const double2* src = reinterpret_cast<const double2*>(a.scratch + s_off[c]);
+            const double2* src = reinterpret_cast<const double2*>(a.scratch + E.off[c]);
             double2 v[4][2];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
@@ -1159,12 +1130,27 @@ static __global__ void __launch_bounds__(256) k_fixup4(const Args2 a, int P) {
             if (q >= nq) continue;
             const int p = 4 * q;
             const int i = p / TX, cx = p - i * TX;
-            const int gy = s_tyi * TY + i;
+            const int gy = E.tyi * TY + i;
             if (gy >= a.my) continue;
+            const int gx0 = E.txi * TX + cx;
+            const long long o0 = obase + (long long)gy * a.mx + gx0;
+            if (gx0 + 3 < a.mx && ((uintptr_t)(a.dst + o0) & 31) == 0) {  // whole aligned quad: one 32-byte access
+                double4* d4 = reinterpret_cast<double4*>(a.dst + o0);
+                double4 r = acc[t];
+                if (a.accumulate) {
+                    const double4 old = *d4;
+                    r.x += old.x;
+                    r.y += old.y;
+                    r.z += old.z;
+                    r.w += old.w;
+                }
+                *d4 = r;
+                continue;
+            }
             const double vv[4] = {acc[t].x, acc[t].y, acc[t].z, acc[t].w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-                const int gx = s_txi * TX + cx + w;
+                const int gx = gx0 + w;
                 if (gx >= a.mx) continue;
                 const long long o = obase + (long long)gy * a.mx + gx;
                 a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + vv[w];
@@ -1459,6 +1445,73 @@ static TileChoice pick_tile(int mx, int my, int P) {
     return best;
 }
 
+// minimum planes per persistent CTA range (see launch_canon_t)
+static long long canon_minlen(long long units, int P, int sms) {
+    const char* ml = getenv("IGALR_MINLEN");  // (experiment knob)
+    if (ml) return std::max(1LL, atoll(ml));
+    return units >= (long long)sms * (2 * P + 2) ? 2 * P + 2 : 1;
+}
+
+// Partial output planes of a canonical launch and their contributors, in CTA order (the same
+// enumeration the kernel's retire/flush code uses: CTA k, segment seg over tile t and input planes
+// [za, zb) writes every zo in [za-P, zb+P) of the mesh, to scratch slot partial_slot(zo, za, zb, P)
+// unless all of zo's input planes [zo-P, zo+P] lie in [za, zb)).  Built once per launch shape and
+// cached in the op (device copy); deterministic.
+static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, const f2::FixEnt** tab, int* n,
+                               cudaStream_t st) {
+    const long long key[9] = {P, a.tyt, a.txt, a.tiles_x, a.tiles_y, a.batch, a.mx, a.my, a.nctas};
+    std::lock_guard<std::mutex> lock(op->fix_mu);
+    for (const auto& c : op->fix_cache)
+        if (std::equal(key, key + 9, c.key)) {
+            *tab = static_cast<const f2::FixEnt*>(c.d_tab);
+            *n = c.n;
+            return cudaSuccess;
+        }
+    std::map<std::pair<long long, int>, f2::FixEnt> ents;
+    const long long TYX = (long long)a.tyt * a.txt;
+    for (int k = 0; k < a.nctas; ++k) {
+        const long long c0 = f2::unit_begin(k, a.units, a.nctas), c1 = f2::unit_begin(k + 1, a.units, a.nctas);
+        int seg = 0;
+        for (long long u = c0; u < c1; ++seg) {
+            const long long tile = u / a.mz;
+            const int za = (int)(u - tile * a.mz);
+            const int zb = (int)std::min((long long)a.mz, (long long)za + (c1 - u));
+            for (int zo = std::max(0, za - P); zo < std::min(a.mz, zb + P); ++zo) {
+                const int lo = std::max(0, zo - P), hi = std::min(a.mz - 1, zo + P);
+                if (lo >= za && hi <= zb - 1) continue;  // complete: written to the output directly
+                f2::FixEnt& E = ents[{tile, zo}];
+                if (E.n == 0) {
+                    long long tt = tile;
+                    E.txi = (int)(tt % a.tiles_x); tt /= a.tiles_x;
+                    E.tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
+                    E.b = (int)tt;
+                    E.zo = zo;
+                }
+                if (E.n >= 2 * 4 + 1) return cudaErrorInvalidConfiguration;
+                E.off[E.n++] = (((long long)k * f2::NSEG + seg) * 4 * P + f2::partial_slot(zo, za, zb, P)) * TYX;
+            }
+            u += zb - za;
+        }
+    }
+    std::vector<f2::FixEnt> v;
+    v.reserve(ents.size());
+    for (auto& kv : ents) v.push_back(kv.second);
+    iga_lr_op::FixCache c;
+    std::copy(key, key + 9, c.key);
+    c.n = (int)v.size();
+    c.d_tab = nullptr;
+    if (!v.empty()) {
+        cudaError_t e = cudaMalloc(&c.d_tab, v.size() * sizeof(f2::FixEnt));
+        // (pageable source: the copy is staged before the call returns, then runs in stream order)
+        if (!e) e = cudaMemcpyAsync(c.d_tab, v.data(), v.size() * sizeof(f2::FixEnt), cudaMemcpyHostToDevice, st);
+        if (e) return e;
+    }
+    op->fix_cache.push_back(c);
+    *tab = static_cast<const f2::FixEnt*>(c.d_tab);
+    *n = c.n;
+    return cudaSuccess;
+}
+
 template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW>
 cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st) {
@@ -1490,7 +1543,10 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long nct = sms;
-    const long long minlen = 2 * P + 2;
+    // CTA ranges of >= 2P+2 planes keep the fixup volume (2P partial planes per range boundary)
+    // small; a mesh with fewer units than that takes one CTA per unit instead (every plane then has
+    // up to 2P+1 contributors, which the table-driven fixup sums): parallelism wins there (c2).
+    const long long minlen = canon_minlen(a.units, P, sms);
     if (a.units / nct < minlen) nct = a.units / minlen;
     if (nct < 1) nct = 1;
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
@@ -1504,10 +1560,19 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
     e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
     if (e) return e;
+    int nfix = 0;
+    const f2::FixEnt* tab = nullptr;
+    if (a.nctas > 1) {
+        e = fixup_table(op, a, P, &tab, &nfix, st);
+        if (e) {
+            cudaFreeAsync(a.scratch, st);
+            return e;
+        }
+    }
     kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a, tmap);
     e = cudaGetLastError();
-    if (!e && a.nctas > 1) {
-        k_fixup4<<<(a.nctas - 1) * 2 * P, 256, 0, st>>>(a, P);
+    if (!e && nfix > 0) {
+        f2::k_fixup_tab<<<nfix, 256, 0, st>>>(a, tab);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
@@ -1567,7 +1632,7 @@ cudaError_t canon_launch_p3(int part, const iga_lr_op* op, const Plan& pl, const
 cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                             int accumulate, int batch, cudaStream_t st);
 
-#ifdef IGALR_CANON_P
+#if defined(IGALR_CANON_P) && IGALR_CANON_P != 99  // (99: experiment TUs instantiate kernels themselves)
 template <class S, int P>
 cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st) {
@@ -1684,6 +1749,19 @@ namespace {
 bool fused2_supported(const iga_lr_op* op) {
     if (op->p[0] != op->p[1] || op->p[0] != op->p[2]) return false;
     return op->p[0] == 3 || op->p[0] == 4;
+}
+
+bool canon_small_grid(const iga_lr_op* op, int batch) {
+    // both parts' persistent grids fit the GPU side by side: launch them concurrently
+    if (!fused2_supported(op)) return false;
+    const int P = op->p[0];
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
+    const long long tx = 32 * tc.qx, ty = (long long)tc.lw * 2 * (4 / tc.qx);
+    const long long units = (op->m[0] + tx - 1) / tx * ((op->m[1] + ty - 1) / ty) * batch * op->m[2];
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 2 * units <= sms;
 }
 
 bool fused2_preferred(const iga_lr_op* op, int batch) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -97,6 +98,17 @@ struct iga_lr_op {
     igalr::Plan plan[igalr::kNumPlans];
     double min_bytes = 0;
     int device = 0;
+    // fixup tables of the canonical kernels, per launch shape (built on first use; fused2_impl.cuh)
+    struct FixCache {
+        long long key[9];
+        void* d_tab;
+        int n;
+    };
+    mutable std::mutex fix_mu;
+    mutable std::vector<FixCache> fix_cache;
+    // side stream for running the mass part beside the stiffness part on small grids (lazily
+    // created under fix_mu; abi.cu run_f2)
+    mutable cudaStream_t side = nullptr;
 };
 
 namespace igalr {
@@ -123,6 +135,7 @@ iga_status prepare_fused(const iga_lr_op* op, Plan* pl);
 void release_fused(Plan* pl);
 bool fused2_supported(const iga_lr_op* op);
 bool fused2_preferred(const iga_lr_op* op, int batch);
+bool canon_small_grid(const iga_lr_op* op, int batch);
 iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part);
 iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part);
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
