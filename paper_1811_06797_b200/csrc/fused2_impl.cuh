@@ -952,12 +952,34 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     yzstage(Qc, step - 2 * P);
                 });
                 if (ret_valid) {
-                    // plane zret is final: write it (or its partial) out and clear its slot
+                    // plane zret is final: write it (or its partial) out and clear its slot.  The
+                    // LW TMEM loads are issued in chunks of 8 with one wait per chunk (a load+wait per
+                    // row serialises LW TMEM round trips)
                     tm_wait_st();
+                    double rv[LW];
+                    static_for<0, (LW + 7) / 8>([&](auto Cc) {
+                        constexpr int c0 = decltype(Cc)::value * 8;
+                        constexpr int cn = LW - c0 < 8 ? LW - c0 : 8;
+                        uint32_t lo[8], hi[8];
+#pragma unroll
+                        for (int q = 0; q < cn; ++q)
+                            asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                                         : "=r"(lo[q]), "=r"(hi[q])
+                                         : "r"(tbase + (c0 + q) * RS::COLS + 2 * jret));
+#pragma unroll
+                        for (int q = cn; q < 8; ++q) lo[q] = hi[q] = 0u;
+                        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                                     : "+r"(lo[0]), "+r"(hi[0]), "+r"(lo[1]), "+r"(hi[1]), "+r"(lo[2]), "+r"(hi[2]),
+                                       "+r"(lo[3]), "+r"(hi[3]), "+r"(lo[4]), "+r"(hi[4]), "+r"(lo[5]), "+r"(hi[5]),
+                                       "+r"(lo[6]), "+r"(hi[6]), "+r"(lo[7]), "+r"(hi[7]));
+#pragma unroll
+                        for (int q = 0; q < cn; ++q) rv[c0 + q] = __hiloint2double(hi[q], lo[q]);
+                    });
+#pragma unroll
+                    for (int i = 0; i < LW; ++i) tm_st1(tbase + i * RS::COLS + 2 * jret, 0.0);
+#pragma unroll
                     for (int i = 0; i < LW; ++i) {
-                        const uint32_t ts = tbase + i * RS::COLS + 2 * jret;
-                        const double val = tm_ld1(ts);
-                        tm_st1(ts, 0.0);
+                        const double val = rv[i];
                         const int gy = y0 + row0 + i;
                         if (gy < a.my && gx < a.mx) {
                             if (ret_complete) {
