@@ -227,7 +227,7 @@ def launches_per_step(info: dict, path: str, kkt: bool) -> int:
     """Our kernels per step: fused v2 = (k_canon + k_fixup) per part; KKT = k_kkt_combos + one mass
     launch over 3 n_t vectors + two accumulating stiffness launches (each with its fixup)."""
     if info.get("fused2_ok") and path != "unfused":
-        return 1 + 2 * 3 if kkt else 4
+        return 1 + 2 * 2 if kkt else 4
     if info["fused_ok"] and path != "unfused":
         return 4 if kkt else 1
     r = info["n_rounds"]

@@ -606,11 +606,19 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
                        !(getenv("IGALR_F2_GENERIC") && getenv("IGALR_F2_GENERIC")[0] == '1');
     if (!s && canon) {
-        // (r_y, r_u, r_lam) = M [b, tau a, c] in one launch over 3 n_t vectors, then
-        // r_y += tau S lambda and r_lam += tau S y (accumulating launches)
+        // (r_y, r_u, r_lam) = M [b, tau a, c] in one launch over 3 n_t vectors, then one
+        // accumulating stiffness launch over 2 n_t vectors: [lambda, y] -> [r_y, r_lam] (a batch
+        // split: vectors n_t.. read y at in and write r_lam at out + 2 blk)
         s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
-        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, n_t, st);
-        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
+        CanonSplit sp;
+        sp.bsplit = n_t;
+        sp.src_jump = -3 * (long long)blk;  // in + 2 blk + b N - 3 blk = in + (b - n_t) N
+        sp.dst_jump = (long long)blk;       // out + b N + blk = out + 2 blk + (b - n_t) N
+        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, 2 * n_t, st, sp);
+        if (s == IGA_EUNSUPPORTED) {  // no split variant for this shape: one launch per segment
+            s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, n_t, st);
+            if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
+        }
     } else if (!s) {
         // r_y = M b + tau S lambda ; r_u = tau M a ; r_lambda = M c + tau S y
         s = iga_lr_apply2(op, abc, in + 2 * blk, out, 1.0, tau, n_t, flags, stream);

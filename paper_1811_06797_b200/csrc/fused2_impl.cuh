@@ -69,6 +69,12 @@ struct Args2 {
     int nctas;
     int txt, tyt;          // tile width / height (fixup)
 };
+// Batch split of a canonical launch (KKT): vectors b >= bsplit read src + b*vol + src_jump and
+// write dst + b*vol + dst_jump (element offsets).  A separate kernel parameter: growing Args2 moves
+// the register-tight p = 4 kernel over the spill cliff.
+struct KSplit {
+    long long bsplit, src_jump, dst_jump;
+};
 
 constexpr int NSEG = 4;    // max segments per CTA (checked on the host)
 
@@ -597,8 +603,8 @@ __host__ __device__ constexpr bool gsync_path() {
 }
 
 // QX of the 4 TMEM lane quadrants tile x (32 columns each); the other 4/QX stack in y.
-template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA>
-__global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const __grid_constant__ CUtensorMap tmap) {
+template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA, bool SPLIT = false>
+__global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const KSplit ks) {
     constexpr int TX = 32 * QX;                 // tile columns (shadows the 128-wide default)
     constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
     using G_ = GeoC<P, TX, TY>;
@@ -674,7 +680,11 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         const int tyi = (int)(tt % a.tiles_y); tt /= a.tiles_y;
         const int b = (int)tt;
         const int x0 = txi * TX, y0 = tyi * TY;
+        // input / output vector bases; SPLIT (KKT): vectors b >= bsplit jump (a compile-time
+        // variant, so the register-tight p = 4 kernels are untouched)
         const long long vb = (long long)b * a.mz * plane;
+        const long long vbs = SPLIT ? vb + (b >= ks.bsplit ? ks.src_jump : 0) : vb;
+        const long long vbd = SPLIT ? vb + (b >= ks.bsplit ? ks.dst_jump : 0) : vb;
         const int gx = x0 + cx;
 
         __syncthreads();
@@ -716,7 +726,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
                     mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
                     double* dstp = vin + buf * VSZ + (cs - cbase);
-                    const double* srcp = a.src + vb + (long long)zp * plane + cs;
+                    const double* srcp = a.src + vbs + (long long)zp * plane + cs;
                     for (int r = rlo; r < rhi; ++r)
                         bulk_g2s(dstp + r * HXP, srcp + (long long)(y0 - P + r) * a.mx, rb, &pbar[buf]);
                     bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes, &pbar[buf]);
@@ -724,7 +734,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 return;
             }
             double* dstp = vin + buf * VSZ;
-            const double* srcp = a.src + vb + (long long)zp * plane;
+            const double* srcp = a.src + vbs + (long long)zp * plane;
             {
                 // (tensor-map boxes would give free OOB zero fill, but starting a box at a
                 // negative coordinate faults on this stack — tools/tma_test.cu — so the halo'd
@@ -983,7 +993,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                         const int gy = y0 + row0 + i;
                         if (gy < a.my && gx < a.mx) {
                             if (ret_complete) {
-                                const long long o = vb + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                const long long o = vbd + (long long)zret * plane + (long long)gy * a.mx + gx;
                                 a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
                             } else {
                                 const int slot = partial_slot(zret, za, zb, P);
@@ -1017,7 +1027,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
                     const bool complete = lo >= za && hi <= zb - 1;
                     if (complete) {
-                        const long long o = vb + (long long)zo * plane + (long long)gy * a.mx + gx;
+                        const long long o = vbd + (long long)zo * plane + (long long)gy * a.mx + gx;
                         a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
                     } else {
                         const int slot = partial_slot(zo, za, zb, P);
@@ -1114,11 +1124,11 @@ struct FixEnt {
     int n, pad;
     long long off[2 * 4 + 1];  // scratch offsets of the contributors (<= 2P+1), CTA order
 };
-static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const FixEnt* __restrict__ tab) {
+static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const FixEnt* __restrict__ tab, const KSplit ks) {
     const FixEnt& E = tab[blockIdx.x];
     const int TY = a.tyt, TX = a.txt;
     const long long plane = (long long)a.mx * a.my;
-    const long long obase = (long long)E.b * a.mz * plane + (long long)E.zo * plane;
+    const long long obase = (long long)E.b * a.mz * plane + (long long)E.zo * plane + (E.b >= ks.bsplit ? ks.dst_jump : 0);
     const int n = E.n;
     const int nq = TY * TX / 4;
     for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * blockDim.x) {
@@ -1534,9 +1544,9 @@ static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, c
     return cudaSuccess;
 }
 
-template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW>
+template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW, bool SPLIT = false>
 cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
-                           int accumulate, int batch, cudaStream_t st) {
+                           int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     using namespace f2;
     constexpr int WPQ = CanonCfg<P>::WPQ;
     constexpr int TXT = 32 * QX, TYT = LW * WPQ * (4 / QX);
@@ -1574,9 +1584,11 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
     a.nctas = (int)nct;
     const size_t sm = smem_bytes_canon<S, P, LW, WPQ, QX, YRES>(a.nrounds);
-    auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA>;
-    CUtensorMap tmap;  // unused (kept in the signature for a future TMA plane path)
-    memset(&tmap, 0, sizeof tmap);
+    auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA, SPLIT>;
+    f2::KSplit ks;
+    ks.bsplit = sp.bsplit;
+    ks.src_jump = sp.src_jump;
+    ks.dst_jump = sp.dst_jump;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
@@ -1591,10 +1603,10 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
             return e;
         }
     }
-    kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a, tmap);
+    kern<<<a.nctas, NW * WPQ * 32, sm, st>>>(a, ks);
     e = cudaGetLastError();
     if (!e && nfix > 0) {
-        f2::k_fixup_tab<<<nfix, 256, 0, st>>>(a, tab);
+        f2::k_fixup_tab<<<nfix, 256, 0, st>>>(a, tab, ks);
         e = cudaGetLastError();
     }
     cudaFreeAsync(a.scratch, st);
@@ -1624,7 +1636,7 @@ size_t canon_smem(int p, int nrounds) {
 
 template <class S, int P, int QX, int LW = CanonCfg<P>::LW>
 cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
-                           int accumulate, int batch, cudaStream_t st) {
+                           int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     const char* s = getenv("IGALR_YRES");
     const bool force_off = s && s[0] == '0';
     const char* t = getenv("IGALR_TMA");
@@ -1633,49 +1645,57 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     // the GSYNC path (TMA && YRES) also bulk-copies plane rows: 16-byte aligned input
     const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
     const bool yres = !force_off && yres_fits<S, P, QX, LW>(pl.canon_nrounds);
+    if (sp.bsplit) {
+        // batch split (KKT stiffness): p = 3 stiffness on the GSYNC path only; otherwise the
+        // caller falls back to one launch per segment
+        if constexpr (P == 3 && std::is_same<S, f2::ShapeStiffA>::value) {
+            if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        }
+        return cudaErrorNotSupported;
+    }
     if constexpr (LW != CanonCfg<P>::LW) {
         // alternative row count: instantiated for the GSYNC path only
-        if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st);
-        return launch_canon_q<S, P, QX>(op, pl, src, dst, scale, accumulate, batch, st);
+        if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        return launch_canon_q<S, P, QX>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
     if (tma) {
-        if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st);
-        return launch_canon_t<S, P, QX, false, true>(op, pl, src, dst, scale, accumulate, batch, st);
+        if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        return launch_canon_t<S, P, QX, false, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
-    if (yres) return launch_canon_t<S, P, QX, true, false>(op, pl, src, dst, scale, accumulate, batch, st);
-    return launch_canon_t<S, P, QX, false, false>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (yres) return launch_canon_t<S, P, QX, true, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    return launch_canon_t<S, P, QX, false, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
 }
 
 }  // namespace
 
 // Per-degree instantiations live in canon_p3.cu / canon_p4.cu (parallel compilation).
 cudaError_t canon_launch_p3(int part, const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
-                            int accumulate, int batch, cudaStream_t st);
+                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp);
 cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
-                            int accumulate, int batch, cudaStream_t st);
+                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp);
 
 #if defined(IGALR_CANON_P) && IGALR_CANON_P != 99  // (99: experiment TUs instantiate kernels themselves)
 template <class S, int P>
 cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
-                             int accumulate, int batch, cudaStream_t st) {
+                             int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
     if constexpr (P == 3) {
-        if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st);
+        if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
-    if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st);
-    if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st);
-    return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st);
+    if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st, sp);
 }
 #define IGALR_CAT2(a, b) a##b
 #define IGALR_CAT(a, b) IGALR_CAT2(a, b)
 cudaError_t IGALR_CAT(canon_launch_p, IGALR_CANON_P)(int part, const iga_lr_op* op, const Plan& pl, const double* src,
-                                                     double* dst, double scale, int accumulate, int batch, cudaStream_t st) {
+                                                     double* dst, double scale, int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     if (part == 0) {
         if (pl.canon_mk == 3)
-            return launch_canon_deg<f2::ShapeMassK<3>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
-        return launch_canon_deg<f2::ShapeMassK<4>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+            return launch_canon_deg<f2::ShapeMassK<3>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        return launch_canon_deg<f2::ShapeMassK<4>, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
-    return launch_canon_deg<f2::ShapeStiffA, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st);
+    return launch_canon_deg<f2::ShapeStiffA, IGALR_CANON_P>(op, pl, src, dst, scale, accumulate, batch, st, sp);
 }
 #endif
 
@@ -1758,9 +1778,10 @@ iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part) {
 }
 
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
-                            int accumulate, int batch, cudaStream_t st) {
-    cudaError_t e = op->p[0] == 3 ? canon_launch_p3(part, op, pl, src, dst, scale, accumulate, batch, st)
-                                  : canon_launch_p4(part, op, pl, src, dst, scale, accumulate, batch, st);
+                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
+    cudaError_t e = op->p[0] == 3 ? canon_launch_p3(part, op, pl, src, dst, scale, accumulate, batch, st, sp)
+                                  : canon_launch_p4(part, op, pl, src, dst, scale, accumulate, batch, st, sp);
+    if (e == cudaErrorNotSupported && sp.bsplit) return IGA_EUNSUPPORTED;  // (no error state)
     if (e) return cuda_error(e, "k_canon");
     return IGA_OK;
 }

@@ -138,8 +138,13 @@ bool fused2_preferred(const iga_lr_op* op, int batch);
 bool canon_small_grid(const iga_lr_op* op, int batch);
 iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part);
 iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part);
+// Batch split of a canonical launch (KKT): vectors b >= bsplit are read at src + b*vol + src_jump
+// and written at dst + b*vol + dst_jump (element offsets).  The default is the plain batch.
+struct CanonSplit {
+    long long bsplit = 0, src_jump = 0, dst_jump = 0;
+};
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
-                            int accumulate, int batch, cudaStream_t st);
+                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp = CanonSplit());
 iga_status apply_fused2_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st);
 iga_status kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, double* tmp, cudaStream_t st);
