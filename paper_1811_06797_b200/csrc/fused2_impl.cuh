@@ -850,12 +850,20 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 for (int e = 0; e < NX; ++e)
 #pragma unroll
                     for (int k = 0; k < BW; ++k) xr[e][k] = xc[(e * TX + cx) * BW + k];
-                double zr[NG][BW];
+                // p = 4 stiffness on the GSYNC path reads the (pre-scaled) z record from shared
+                // memory in the Z stage (broadcast loads) instead of holding NG x BW doubles in
+                // registers: its sweep sits at the 255-register cliff.  The freed registers take the
+                // pair ratios and an early TMEM ring load (c5 stiffness 1.86 -> 1.77 ms; the mass
+                // shape is faster with register-resident coefficients)
+                constexpr bool ZSMEM = GSYNC && P >= 4 && std::is_same<S, ShapeStiffA>::value;
+                double zr[ZSMEM ? 1 : NG][ZSMEM ? 1 : BW];
+                if constexpr (!ZSMEM) {
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    const double gsc = GSYNC ? 1.0 : R.gs[g];  // (the GSYNC z record is pre-scaled)
+                    for (int g = 0; g < NG; ++g) {
+                        const double gsc = GSYNC ? 1.0 : R.gs[g];  // (the GSYNC z record is pre-scaled)
 #pragma unroll
-                    for (int j = 0; j < BW; ++j) zr[g][j] = zc[g * BW + j] * gsc;
+                        for (int j = 0; j < BW; ++j) zr[g][j] = zc[g * BW + j] * gsc;
+                    }
                 }
                 double pc[NPAIR];
 #pragma unroll
@@ -896,7 +904,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     uint32_t rr[RS::DBL * 2];
                     // TMEM load in flight during the Y stage (p=3); p=4 issues it after the Y stage:
                     // its 18 registers would push the Y stage into spills
-                    constexpr bool EARLY_RING = (P <= 3);
+                    constexpr bool EARLY_RING = (P <= 3) || ZSMEM;
                     if constexpr (EARLY_RING) ring_issue<BW>(tp, rr);
                     double G[NG];
 #pragma unroll
@@ -926,7 +934,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #pragma unroll
                                 for (int k = 1; k < BW; ++k) u = fma(yv[k], w[e][(Q + 1 + k) % BW], u);
                                 // (p=4: the ratio is re-read from shared memory: register pressure)
-                                G[g] = fma(P <= 3 ? pc[j] : R.pc[j], u, G[g]);
+                                G[g] = fma((P <= 3 || ZSMEM) ? pc[j] : R.pc[j], u, G[g]);
                             }
                         }
                     }
@@ -936,7 +944,8 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #pragma unroll
                     for (int g = 0; g < NG; ++g)
 #pragma unroll
-                        for (int j = 0; j < BW; ++j) ring[j] = fma(zr[g][j], G[g], ring[j]);
+                        for (int j = 0; j < BW; ++j)
+                            ring[j] = fma(ZSMEM ? zc[g * BW + j] : zr[ZSMEM ? 0 : g][ZSMEM ? 0 : j], G[g], ring[j]);
                     ring_st<BW>(tp, ring);
                 };
                 constexpr int HYW = LW + 2 * P;        // rows swept by this warp
