@@ -29,6 +29,10 @@
 
 #include "internal.h"
 
+#ifndef IGALR_ZSMEM_P
+#define IGALR_ZSMEM_P 4  // (experiment knob: smallest degree whose stiffness kernel reads z from smem)
+#endif
+
 namespace igalr {
 namespace f2 {
 
@@ -175,31 +179,36 @@ __device__ __forceinline__ void tm_st1(uint32_t taddr, double v) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// ring slots per point, padded to a multiple of 8 doubles (x16 loads) or +2 (x4 tail)
-template <int BW>
+// ring slots per point, padded to a multiple of 8 doubles (x16 loads) or +2 (x4 tail).  TIGHT
+// (canonical kernel): an odd tail below 5 doubles ends in one x2 access instead of padding, so
+// p = 4 (2P+1 = 9) stores 9 doubles (18 columns) per point instead of 10
+template <int BW, bool TIGHT = false>
 struct RingShape {
     static constexpr int REM = BW % 8;
     static constexpr int N16 = BW / 8 + (REM >= 5 ? 1 : 0);     // number of x16 chunks (8 doubles)
-    static constexpr int N4 = (REM >= 5 || REM == 0) ? 0 : (REM + 1) / 2;  // x4 chunks (2 doubles)
-    static constexpr int DBL = N16 * 8 + N4 * 2;  // doubles stored per point
-    static constexpr int COLS = DBL * 2;          // TMEM columns per point
+    static constexpr int N4 = (REM >= 5 || REM == 0) ? 0 : (TIGHT ? REM / 2 : (REM + 1) / 2);  // x4 chunks
+    static constexpr int N2 = (TIGHT && REM < 5 && (REM & 1)) ? 1 : 0;  // x2 chunk (1 double)
+    static constexpr int DBL = N16 * 8 + N4 * 2 + N2;  // doubles stored per point
+    static constexpr int COLS = DBL * 2;               // TMEM columns per point
 };
 
-template <int BW>
+template <int BW, bool TIGHT = false>
 __device__ __forceinline__ void ring_ld(uint32_t t, double* v) {
-    using RS = RingShape<BW>;
+    using RS = RingShape<BW, TIGHT>;
 #pragma unroll
     for (int c = 0; c < RS::N16; ++c) tm_ld16(t + c * 16, v + c * 8);
 #pragma unroll
     for (int c = 0; c < RS::N4; ++c) tm_ld4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+    if constexpr (RS::N2) v[RS::DBL - 1] = tm_ld1(t + RS::COLS - 2);
 }
-template <int BW>
+template <int BW, bool TIGHT = false>
 __device__ __forceinline__ void ring_st(uint32_t t, const double* v) {
-    using RS = RingShape<BW>;
+    using RS = RingShape<BW, TIGHT>;
 #pragma unroll
     for (int c = 0; c < RS::N16; ++c) tm_st16(t + c * 16, v + c * 8);
 #pragma unroll
     for (int c = 0; c < RS::N4; ++c) tm_st4(t + RS::N16 * 16 + c * 4, v + RS::N16 * 8 + c * 2);
+    if constexpr (RS::N2) tm_st1(t + RS::COLS - 2, v[RS::DBL - 1]);
 }
 
 template <int B, int E, class F>
@@ -211,9 +220,9 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 
 // split TMEM ring load: issue now, wait (tied to the registers) when the values are needed
-template <int BW>
+template <int BW, bool TIGHT = false>
 __device__ __forceinline__ void ring_issue(uint32_t t, uint32_t* r) {
-    using RS = RingShape<BW>;
+    using RS = RingShape<BW, TIGHT>;
 #pragma unroll
     for (int c = 0; c < RS::N16; ++c) {
         uint32_t* q = r + c * 16;
@@ -230,16 +239,27 @@ __device__ __forceinline__ void ring_issue(uint32_t t, uint32_t* r) {
                      : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
                      : "r"(t + RS::N16 * 16 + c * 4));
     }
+    if constexpr (RS::N2) {
+        uint32_t* q = r + RS::N16 * 16 + RS::N4 * 4;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                     : "=r"(q[0]), "=r"(q[1])
+                     : "r"(t + RS::COLS - 2));
+    }
 }
-template <int BW>
+template <int BW, bool TIGHT = false>
 __device__ __forceinline__ void ring_wait(uint32_t* r, double* v) {
-    using RS = RingShape<BW>;
+    using RS = RingShape<BW, TIGHT>;
     static_assert(RS::DBL * 2 <= 24, "ring_wait handles up to 24 registers");
     if constexpr (RS::DBL * 2 == 16) {
         asm volatile("tcgen05.wait::ld.sync.aligned;"
                      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
                        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
                        "+r"(r[15]));
+    } else if constexpr (RS::DBL * 2 == 18) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                       "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                       "+r"(r[15]), "+r"(r[16]), "+r"(r[17]));
     } else if constexpr (RS::DBL * 2 == 20) {
         asm volatile("tcgen05.wait::ld.sync.aligned;"
                      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
@@ -609,10 +629,12 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
     using G_ = GeoC<P, TX, TY>;
     constexpr int BW = G_::BW, BWP = G_::BWP, HY = G_::HY;
+    // 9-double ring (x16 + x2 accesses) when the padded 10-double ring would not fit this LW
+    constexpr bool TIGHTR = LW * RingShape<BW>::COLS * WPQ > 512;
     constexpr int HXP = G_::HXP, PADL = G_::PADL;
     constexpr int VSZ = (HY * G_::HXP + 15) & ~15;  // doubles per plane buffer (128-B aligned)
     constexpr int NX = S::NX, NY = S::NY, NG = S::NG, NPAIR = S::NPAIR;
-    using RS = RingShape<BW>;
+    using RS = RingShape<BW, TIGHTR>;
     using RoundT = RoundC<S>;
     static_assert(LW * RS::COLS * WPQ <= 512, "ring does not fit in TMEM");
 
@@ -710,7 +732,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             double zero[RS::DBL];
 #pragma unroll
             for (int k = 0; k < RS::DBL; ++k) zero[k] = 0.0;
-            for (int i = 0; i < LW; ++i) ring_st<BW>(tbase + i * RS::COLS, zero);
+            for (int i = 0; i < LW; ++i) ring_st<BW, TIGHTR>(tbase + i * RS::COLS, zero);
         }
 
         auto stage_plane = [&](int zp, int buf) {
@@ -855,7 +877,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 // registers: its sweep sits at the 255-register cliff.  The freed registers take the
                 // pair ratios and an early TMEM ring load (c5 stiffness 1.86 -> 1.77 ms; the mass
                 // shape is faster with register-resident coefficients)
-                constexpr bool ZSMEM = GSYNC && P >= 4 && std::is_same<S, ShapeStiffA>::value;
+                constexpr bool ZSMEM = GSYNC && P >= IGALR_ZSMEM_P && std::is_same<S, ShapeStiffA>::value;
                 double zr[ZSMEM ? 1 : NG][ZSMEM ? 1 : BW];
                 if constexpr (!ZSMEM) {
 #pragma unroll
@@ -905,7 +927,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     // TMEM load in flight during the Y stage (p=3); p=4 issues it after the Y stage:
                     // its 18 registers would push the Y stage into spills
                     constexpr bool EARLY_RING = (P <= 3) || ZSMEM;
-                    if constexpr (EARLY_RING) ring_issue<BW>(tp, rr);
+                    if constexpr (EARLY_RING) ring_issue<BW, TIGHTR>(tp, rr);
                     double G[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) G[g] = 0.0;
@@ -939,14 +961,14 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                         }
                     }
                     double ring[RS::DBL];
-                    if constexpr (!EARLY_RING) ring_issue<BW>(tp, rr);
-                    ring_wait<BW>(rr, ring);
+                    if constexpr (!EARLY_RING) ring_issue<BW, TIGHTR>(tp, rr);
+                    ring_wait<BW, TIGHTR>(rr, ring);
 #pragma unroll
                     for (int g = 0; g < NG; ++g)
 #pragma unroll
                         for (int j = 0; j < BW; ++j)
                             ring[j] = fma(ZSMEM ? zc[g * BW + j] : zr[ZSMEM ? 0 : g][ZSMEM ? 0 : j], G[g], ring[j]);
-                    ring_st<BW>(tp, ring);
+                    ring_st<BW, TIGHTR>(tp, ring);
                 };
                 constexpr int HYW = LW + 2 * P;        // rows swept by this warp
                 constexpr int NFULL = (HYW - BW) / BW;  // full blocks after block 0
@@ -1021,7 +1043,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         for (int i = 0; i < LW; ++i) {
             const uint32_t tp = tbase + i * RS::COLS;
             double ring[RS::DBL];
-            ring_ld<BW>(tp, ring);
+            ring_ld<BW, TIGHTR>(tp, ring);
             const int gy = y0 + row0 + i;
 #pragma unroll
             for (int s = 0; s < 2 * P; ++s) {
@@ -1467,8 +1489,10 @@ struct TileChoice {
 };
 static TileChoice pick_tile(int mx, int my, int P) {
     const int LW0 = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
-    TileChoice cand[4] = {{4, LW0}, {2, LW0}, {1, LW0}, {2, 12}};
-    const int ncand = (P == 3) ? 4 : 3;
+    // p = 3 also weighs 48-row tiles (LW 12, QX 2); p = 4 weighs LW 13 (26-row tiles, 234 of a
+    // warp's 256 TMEM columns with the 9-double ring): 256 rows tile as 10 x 26 instead of 11 x 24
+    TileChoice cand[4] = {{4, LW0}, {2, LW0}, {1, LW0}, {P == 3 ? 2 : 4, P == 3 ? 12 : 13}};
+    const int ncand = 4;
     TileChoice best = cand[0];
     double bc = 1e30;
     for (int i = 0; i < ncand; ++i) {
@@ -1690,6 +1714,9 @@ cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* 
     const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
     if constexpr (P == 3) {
         if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    }
+    if constexpr (P == 4) {
+        if (tc.lw == 13) return launch_canon_q<S, P, 4, 13>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
     if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st, sp);

@@ -176,6 +176,22 @@ def test_full_size_sampled_rows(env, cfgname):
         assert rel(gm, rm) <= TOL and rel(gs, rs) <= TOL
 
 
+@pytest.mark.parametrize("n,batch", [(104, 1), (101, 2)])
+def test_p4_26row_tiles_sampled_rows(env, n, batch):
+    """p = 4 meshes whose y extent tiles best in 26-row tiles (LW 13, the 9-double TMEM ring):
+    n = 104 (4 full tiles) and n = 101 (ragged last tile), sampled rows vs the oracle."""
+    torch, igalr, workloads = env
+    cfg = synth.scaled(synth.CONFIGS["c5"], n, batch=batch)
+    knots, w, x = synth.draw_problem(cfg)
+    op = workloads.build_operator(cfg, w)
+    P = oracle.problem_from_config(cfg, w)
+    yM, yS = gpu_apply(env, op, x, "auto")
+    for b in range(batch):
+        rows = sample_rows(P.dims, 200, 300 + b, cfg.p)
+        rm, rs = oracle.apply_rows(P, x[b], rows)
+        assert rel(yM[b].ravel()[rows], rm) <= TOL and rel(yS[b].ravel()[rows], rs) <= TOL
+
+
 @pytest.mark.parametrize("cfgname", ["c2", "c3"])
 def test_invariants_on_gpu(env, cfgname):
     """P4 (1'M1 = int omega) and P5 (S 1 = 0) on the GPU output, nq = 10 so the rule is exact."""
