@@ -75,7 +75,7 @@ def _L():
         lib.orc_quad_nodes.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_int, D, I64]
         lib.orc_csr_nnz.argtypes = [I, I, ctypes.c_int]
         lib.orc_csr_nnz.restype = ctypes.c_int64
-        common = [I, I, D, D, D, ctypes.c_int, ctypes.c_int, D, I, D, ctypes.c_int]
+        common = [I, I, D, D, D, ctypes.c_int, ctypes.c_int, D, I, D, ctypes.c_int, D]
         lib.orc_assemble_csr.argtypes = common + [I64, I32, D, D]
         lib.orc_spmv.argtypes = [ctypes.c_int64, I64, I32, D, D, D]
         lib.orc_apply_matfree.argtypes = common + [D, D, D]
@@ -149,6 +149,10 @@ class Problem:
     mass_terms: Optional[np.ndarray]
     q_terms: Optional[List[np.ndarray]]
     dirichlet: bool = False
+    # optional general weights at every tensor quadrature point: [10, Gz, Gy, Gx] (omega, then
+    # q_kl at 1 + k*3 + l), G_d = (nonempty spans) * nq along direction d in the order of
+    # quad_nodes(); given => used instead of the separable closed-form terms
+    weights3d: Optional[np.ndarray] = None
     _c: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
@@ -169,6 +173,11 @@ class Problem:
                              dtype=np.int32)
         cat = [np.asarray(q, dtype=np.float64).reshape(-1, TERM_WIDTH) for q in qs if q is not None and len(q)]
         self._tq = np.ascontiguousarray(np.concatenate(cat, 0)) if cat else np.zeros((1, TERM_WIDTH))
+        if self.weights3d is not None:
+            g = [len(quad_nodes(self.knots[d], self.p[d], self.nq)) for d in range(3)]
+            w3 = np.ascontiguousarray(self.weights3d, dtype=np.float64)
+            assert w3.shape == (10, g[2], g[1], g[0]), (w3.shape, g)
+            self._w3 = w3
 
     @property
     def n(self):
@@ -186,7 +195,8 @@ class Problem:
 
     def _args(self):
         return (_ip(self._n), _ip(self._p), _dp(self.knots[0]), _dp(self.knots[1]), _dp(self.knots[2]),
-                self.nq, self._ntm, _dp(self._tm), _ip(self._ntq), _dp(self._tq), int(self.dirichlet))
+                self.nq, self._ntm, _dp(self._tm), _ip(self._ntq), _dp(self._tq), int(self.dirichlet),
+                _dp(self._w3) if self.weights3d is not None else None)
 
 
 def problem_from_config(cfg, weights, n: Optional[int] = None, nq: Optional[int] = None) -> Problem:

@@ -229,12 +229,16 @@ typedef struct {
        fm[d][r*nn_d + g] = 1 + amp sin(k pi t_g + phi) of mass term r, fq[b][d][...] likewise */
     double* fm[3];
     double* fq[9][3];
+    /* optional general (non-separable) weights tabulated at every tensor quadrature point:
+       w3[c][gz][gy][gx], c = 0 omega, c = 1 + k*3 + l q_kl (NULL => the separable closed form) */
+    const double* w3;
 } orc_prob;
 
 static int orc_prob_build(orc_prob* P, const int* n, const int* p, const double* const* knots, int nq,
                           int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
-                          int dirichlet) {
+                          int dirichlet, const double* w3) {
     memset(P, 0, sizeof(*P));
+    P->w3 = w3;
     for (int d = 0; d < 3; ++d) {
         if (orc_tab_build(&P->T[d], knots[d], n[d], p[d], nq)) return 1;
         if (dirichlet) {
@@ -290,6 +294,12 @@ static void orc_prob_free(orc_prob* P) {
    omega(x) = sum_r coef_r f_r^x(x) f_r^y(y) f_r^z(z)  (separable closed form) */
 static void orc_point_weights(const orc_prob* P, int gx, int gy, int gz, double* om, double* q) {
     const int nx = P->T[0].ne * P->T[0].nq, ny = P->T[1].ne * P->T[1].nq, nz = P->T[2].ne * P->T[2].nq;
+    if (P->w3) { /* tabulated general weights (the geometry's omega and Q at the point) */
+        const size_t np = (size_t)nx * ny * nz, at = ((size_t)gz * ny + gy) * nx + gx;
+        *om = P->w3[at];
+        for (int b = 0; b < 9; ++b) q[b] = P->w3[(size_t)(1 + b) * np + at];
+        return;
+    }
     double s = 0.0;
     for (int r = 0; r < P->nt_m; ++r)
         s += P->terms_m[(size_t)r * ORC_TERM] * P->fm[0][(size_t)r * nx + gx] * P->fm[1][(size_t)r * ny + gy] *
@@ -355,10 +365,10 @@ int64_t orc_csr_nnz(const int* n, const int* p, int dirichlet) {
  */
 int orc_assemble_csr(const int* n, const int* p, const double* kx, const double* ky, const double* kz,
                      int nq, int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
-                     int dirichlet, int64_t* rowptr, int32_t* colidx, double* valM, double* valS) {
+                     int dirichlet, const double* w3, int64_t* rowptr, int32_t* colidx, double* valM, double* valS) {
     const double* knots[3] = {kx, ky, kz};
     orc_prob P;
-    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet)) {
+    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3)) {
         orc_prob_free(&P);
         return 1;
     }
@@ -521,10 +531,10 @@ static inline void orc_point_test(const orc_prob* P, int ex, int ey, int ez, int
    touch disjoint rows, so each y_i is summed in a fixed order. */
 int orc_apply_matfree(const int* n, const int* p, const double* kx, const double* ky, const double* kz, int nq,
                       int nt_m, const double* terms_m, const int* nt_q, const double* terms_q, int dirichlet,
-                      const double* x, double* yM, double* yS) {
+                      const double* w3, const double* x, double* yM, double* yS) {
     const double* knots[3] = {kx, ky, kz};
     orc_prob P;
-    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet)) {
+    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3)) {
         orc_prob_free(&P);
         return 1;
     }
@@ -585,10 +595,10 @@ int orc_apply_matfree(const int* n, const int* p, const double* kx, const double
 /* the same bilinear form for selected rows only (kept-DoF linear indices) */
 int orc_apply_rows(const int* n, const int* p, const double* kx, const double* ky, const double* kz, int nq,
                    int nt_m, const double* terms_m, const int* nt_q, const double* terms_q, int dirichlet,
-                   const double* x, int64_t nrows, const int64_t* rows, double* yM, double* yS) {
+                   const double* w3, const double* x, int64_t nrows, const int64_t* rows, double* yM, double* yS) {
     const double* knots[3] = {kx, ky, kz};
     orc_prob P;
-    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet)) {
+    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3)) {
         orc_prob_free(&P);
         return 1;
     }
