@@ -480,3 +480,57 @@ def test_kkt_nt1_reduces_to_single_step():
     assert np.allclose(out[0, 0], t * Md @ y + A.T @ lam, atol=1e-14)
     assert np.allclose(out[1, 0], t * b * Md @ u - t * Md @ lam, atol=1e-15)
     assert np.allclose(out[2, 0], A @ y - t * Md @ u, atol=1e-14)
+
+
+# ------------------------------------------------------------- general (tabulated) weights
+def _tab3(P, fields):
+    """A weight field evaluated on the oracle's own tensor quadrature grid."""
+    nodes = [oracle.quad_nodes(P.knots[d], P.p[d], P.nq) for d in range(3)]
+    return fields(nodes[0], nodes[1], nodes[2])
+
+
+def test_weights3d_separable_equals_closed_form():
+    """The tabulated-weight path (Eqs. (massMatrix)/(stiffnessMatrix), with
+    omega and Q given at every 3D point) reproduces the closed-form separable path when the table
+    holds the same separable weights."""
+    cfg = synth.scaled(synth.CONFIGS["c2"], 7)
+    w = synth.draw_weights(cfg)
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+
+    def sep(terms):
+        def f(x, y, z):
+            out = np.zeros((len(z), len(y), len(x)))
+            for T in np.asarray(terms).reshape(-1, synth.TERM_WIDTH):
+                fx, fy, fz = (1.0 + T[1 + 3 * d] * np.sin(T[2 + 3 * d] * np.pi * t + T[3 + 3 * d])
+                              for d, t in enumerate((x, y, z)))
+                out += T[0] * fz[:, None, None] * fy[None, :, None] * fx[None, None, :]
+            return out
+        return f
+
+    qb = w.q_block_terms()
+    w3 = np.zeros((10,) + _tab3(P, sep(w.mass)).shape)
+    w3[0] = _tab3(P, sep(w.mass))
+    for b in range(9):
+        if qb[b] is not None and len(qb[b]):
+            w3[1 + b] = _tab3(P, sep(qb[b]))
+    P3 = oracle.Problem(knots=P.knots, p=P.p, nq=P.nq, mass_terms=None, q_terms=None, weights3d=w3)
+    M3, S3 = oracle.assemble_csr(P3)
+    assert abs(M3 - M).max() <= 1e-15 * abs(M).max()
+    assert abs(S3 - S).max() <= 1e-15 * abs(S).max()
+
+
+def test_weights3d_annulus_volume_and_constants():
+    """Quarter annulus with exact geometry weights omega = |det grad G| and
+    Q = (grad G^T grad G)^-1 |det grad G|: 1'M1 = physical volume (partition of
+    unity; omega is linear in s, so the 5-point rule is exact) and S 1 = 0."""
+    from synth.geometry import QuarterAnnulus, refinement_knots
+    g = QuarterAnnulus()
+    kn = refinement_knots(2, 3)
+    P = oracle.Problem(knots=[kn] * 3, p=[2] * 3, nq=5, mass_terms=None, q_terms=None,
+                       weights3d=_tab3(oracle.Problem(knots=[kn] * 3, p=[2] * 3, nq=5, mass_terms=None,
+                                                      q_terms=None), g.fields))
+    M, S = oracle.assemble_csr(P)
+    one = np.ones(P.ndof)
+    assert abs(one @ (M @ one) - g.volume) <= 1e-13 * g.volume
+    assert np.abs(S @ one).max() <= 1e-13 * abs(S).max()
