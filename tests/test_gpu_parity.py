@@ -389,6 +389,29 @@ def test_kkt_full_vs_oracle(env, path, n, nt):
     assert rel(got, ref) <= TOL
 
 
+@pytest.mark.parametrize("p,n,nt", [(4, 12, 3), (3, 11, 4)])
+def test_kkt_batch_split_and_fallback(env, p, n, nt):
+    """The KKT's stiffness part runs as one batch-split launch ([lambda, y] -> [r_y, r_lam]) where a
+    split kernel variant exists (p = 3) and as one launch per block otherwise (p = 4): both match
+    the oracle's rows of Eq. (KKTSystem)."""
+    torch, igalr, workloads = env
+    import dataclasses
+    cfg = dataclasses.replace(synth.scaled(synth.CONFIGS["c4"], n, n_t=nt), p=p)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    m = n - 2
+    X = np.random.default_rng(7 * n + nt).standard_normal((3, nt, m, m, m))
+    ref = oracle.kkt_apply_csr(M, S, X, cfg.tau, cfg.beta)
+    Xd = torch.from_numpy(X).cuda()
+    out = torch.empty_like(Xd)
+    op.kkt_apply(Xd, out, nt, cfg.tau, cfg.beta)
+    got = out.cpu().numpy()
+    for blk in range(3):
+        assert rel(got[blk], ref[blk]) <= TOL
+
+
 def test_kkt_c4_full_size_sampled(env):
     torch, igalr, workloads = env
     cfg = synth.CONFIGS["c4"]
