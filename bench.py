@@ -313,6 +313,51 @@ def time_kkt_solve(rtol: float = 1e-8):
             "prec_setup_s": t1 - t0, "rel_residual_2norm": rel2}
 
 
+def time_tt(ranks=(20, 20), reps: int = 50):
+    """NEXT-3: the reduced-system matvec of Block AMEn (Eq. (KKT_red)) on the c4 operator:
+    interfaces of the middle site (y) for TT cores of ranks (R1, R2), then
+    y = sum_t c_t (L_t (x) K_t^y (x) R_t) x on a local core [R1][m][R2] (stiffness, the largest
+    term set), and one A v of a TT vector; CUDA-event times on one stream."""
+    import torch
+    from paper_1811_06797_b200 import workloads
+    cfg = synth.CONFIGS["c4"]
+    op = workloads.build_operator(cfg, synth.draw_weights(cfg))
+    mx, my, mz = op.dims
+    R1, R2 = ranks
+    g = torch.Generator(device="cuda").manual_seed(3)
+    gz = torch.randn((mz, R1), dtype=torch.float64, device="cuda", generator=g)
+    gy = torch.randn((R1, my, R2), dtype=torch.float64, device="cuda", generator=g)
+    gx = torch.randn((R2, mx), dtype=torch.float64, device="cuda", generator=g)
+    T = len(op.terms(1)[1])
+    L = torch.empty((T, R1, R1), dtype=torch.float64, device="cuda")
+    R = torch.empty((T, R2, R2), dtype=torch.float64, device="cuda")
+    x = torch.randn((R1, my, R2), dtype=torch.float64, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    wz = torch.empty((T, mz, R1), dtype=torch.float64, device="cuda")
+    wy = torch.empty((T, R1, my, R2), dtype=torch.float64, device="cuda")
+    wx = torch.empty((T, R2, mx), dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    t_if = timed(lambda: op.tt_interfaces(1, 1, gz, gy, gx, L, R))
+    t_loc = timed(lambda: op.tt_local_apply(1, 1, L, R, x, y))
+    t_kron = timed(lambda: op.tt_kron_apply(1, gz, gy, gx, wz, wy, wx))
+    p = op.info_dict()["p"][1]
+    flops_loc = 2.0 * T * R1 * my * R2 * (R2 + (2 * p + 1) + R1)
+    return {"workload": "c4_tt_local_apply (Block-AMEn reduced matvec, site y)", "terms": T, "ranks": [R1, R2],
+            "local_unknowns": R1 * my * R2, "interfaces_ms": t_if, "local_apply_ms": t_loc,
+            "local_apply_gflops": flops_loc / (t_loc * 1e-3) / 1e9, "tt_kron_apply_ms": t_kron}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -403,6 +448,10 @@ def main():
                 torch.cuda.empty_cache()
             except Exception as e:  # report, never hide
                 extra[other] = {"error": repr(e)}
+        try:
+            extra["tt"] = time_tt()
+        except Exception as e:  # report, never hide
+            extra["tt"] = {"error": repr(e)}
         try:
             extra["c4_solve"] = time_kkt_solve()
         except Exception as e:  # report, never hide

@@ -231,6 +231,45 @@ iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info);
 iga_status iga_lr_export_factor(const iga_lr_op* op, int32_t dir, int32_t factor_id, double* host_band,
                                 int32_t* pattern, int32_t* table);
 
+/* ---- NEXT-3: the Kronecker operators on tensor-train vectors ----------
+   A 3D TT vector (Eq. (tt)) with ranks (R1, R2) is three DEVICE fp64 cores in
+   the paper's order (slowest direction first):
+       Gz [n_z][R1],  Gy [R1][n_y][R2],  Gx [R2][n_x]
+   v(iz, iy, ix) = sum_{a,b} Gz[iz][a] Gy[a][iy][b] Gx[b][ix]   (extents m_d of the op).
+   The op is a sum of T Kronecker terms c_t Az_t (x) Ay_t (x) Ax_t of one part
+   (part 0 = mass M, 1 = stiffness K; Eqs. (massFinal)/(stiffnessFinal)).
+
+   iga_lr_terms: the T terms of `part` (the op's deduplicated, r-major term list): n_terms,
+     and if non-NULL, HOST fid[t*3 + d] = factor id in direction d (0 x, 1 y, 2 z; see
+     iga_lr_export_factor) and coef[t].  IGA_ESTATE if the op lacks the part.
+
+   iga_tt_kron_apply: w = A v for a TT vector v, exactly, as T TT terms with v's ranks
+     (the rank-(T R1, T R2) TT of w is their block concatenation):
+       Wz [T][n_z][R1] = c_t Az_t Gz,  Wy [T][R1][n_y][R2] = Ay_t Gy,  Wx [T][R2][n_x] = Ax_t Gx
+     (mode products along the physical index; w = sum_t Wz[t] Wy[t] Wx[t]).  DEVICE in/out,
+     outputs must not alias inputs.
+
+   iga_tt_interfaces: the frame interfaces of site `site` (0 x, 1 y, 2 z) for every term:
+     the projection F_{!=d}^T A F_{!=d} of Eq. (KKT_red) with the frame
+     matrix of Eq. (frame) equals sum_t c_t L_t (x) A^(d)_t (x) R_t, with
+       L_t [Rl][Rl] = contraction of the cores left of d (slower directions) with A_t there,
+       R_t [Rr][Rr] = the same for the cores right of d (faster directions);
+     Rl = 1 (site z), R1 (y), R2 (x); Rr = R1 (z), R2 (y), 1 (x).  L, R: DEVICE [T][..][..].
+     The coefficient c_t is not folded in.  (Orthogonality of the frame is the caller's.)
+
+   iga_tt_local_apply: y = (sum_t c_t L_t (x) A^(d)_t (x) R_t) x for a local core
+     x, y [Rl][m_d][Rr] (the reduced-system matvec of Eq. (KKT_red)); DEVICE, no aliasing.
+   Errors: IGA_EINVAL (NULL pointers, ranks < 1, site outside 0..2), IGA_ESTATE (missing part),
+   IGA_ECUDA. */
+iga_status iga_lr_terms(const iga_lr_op* op, int32_t part, int32_t* n_terms, int32_t* fid, double* coef);
+iga_status iga_tt_kron_apply(const iga_lr_op* op, int32_t part, int32_t R1, int32_t R2, const double* gz,
+                             const double* gy, const double* gx, double* wz, double* wy, double* wx, void* stream);
+iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, int32_t R1, int32_t R2,
+                             const double* gz, const double* gy, const double* gx, double* L, double* R,
+                             void* stream);
+iga_status iga_tt_local_apply(const iga_lr_op* op, int32_t part, int32_t site, int32_t Rl, int32_t Rr,
+                              const double* L, const double* R, const double* x, double* y, void* stream);
+
 /* Human-readable message of the last failing call on this thread ("" if none). */
 const char* iga_last_error(void);
 

@@ -509,3 +509,37 @@ def weight_lowrank(nodes, tilde_knots, tilde_p, samples: np.ndarray, eps: float)
             for d, f in ((2, G1[:, r1]), (1, G2[r1, :, r2]), (0, G3[r2, :])):
                 tabs[d][r] = E[d] @ np.linalg.solve(B[d], f)
     return tabs, (R1, R2)
+
+
+# ------------------------------------------------------------------ TT vectors (NEXT-3)
+# Plain definitions for checking the library's TT entry points; 3D, cores in
+# the paper's order (slowest direction first): gz [mz, R1], gy [R1, my, R2], gx [R2, mx].
+def tt_full(gz: np.ndarray, gy: np.ndarray, gx: np.ndarray) -> np.ndarray:
+    """Eq. (tt) (PAPER.md:346-349): v(iz, iy, ix) = sum_{a,b} gz[iz, a] gy[a, iy, b] gx[b, ix]."""
+    return np.einsum("za,ayb,bx->zyx", gz, gy, gx)
+
+
+def tt_frame(gz: np.ndarray, gy: np.ndarray, gx: np.ndarray, site: int) -> np.ndarray:
+    """Frame matrix F_{!=d} of Eq. (frame), dense, rows (iz, iy, ix), columns
+    (r_{d-1}, j_d, r_d) row-major; site 0 = x, 1 = y, 2 = z (d = 3, 2, 1 in the paper)."""
+    mz, R1 = gz.shape
+    _, my, R2 = gy.shape
+    mx = gx.shape[1]
+    if site == 1:   # F[(iz,iy,ix),(a,jy,b)] = gz[iz,a] delta(iy,jy) gx[b,ix]
+        F = np.einsum("za,yj,bx->zyxajb", gz, np.eye(my), gx)
+        return F.reshape(mz * my * mx, R1 * my * R2)
+    if site == 2:   # F[(iz,iy,ix),(jz,a)] = delta(iz,jz) sum_b gy[a,iy,b] gx[b,ix]
+        right = np.einsum("ayb,bx->ayx", gy, gx)
+        F = np.einsum("zj,ayx->zyxja", np.eye(mz), right)
+        return F.reshape(mz * my * mx, mz * R1)
+    # site 0: F[(iz,iy,ix),(b,jx)] = sum_a gz[iz,a] gy[a,iy,b] delta(ix,jx)
+    left = np.einsum("za,ayb->zyb", gz, gy)
+    F = np.einsum("zyb,xj->zyxbj", left, np.eye(mx))
+    return F.reshape(mz * my * mx, R2 * mx)
+
+
+def tt_project(A, gz, gy, gx, site: int) -> np.ndarray:
+    """The projected matrix F_{!=d}^T A F_{!=d} of Eq. (KKT_red), A dense or
+    sparse over the row-major (z, y, x) DoFs."""
+    F = tt_frame(gz, gy, gx, site)
+    return F.T @ (A @ F)

@@ -37,7 +37,8 @@ ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "i
                "iga_kkt_apply", "iga_lr_apply_host", "iga_kkt_apply_host", "iga_lr_info", "iga_lr_export_factor",
                "iga_last_error", "iga_version", "iga_kkt_minres", "iga_kkt_prec_create", "iga_kkt_prec_destroy",
                "iga_kkt_prec_apply", "iga_kkt_prec_info", "iga_greville", "iga_weight_lowrank",
-               "iga_weight_lowrank_sep", "iga_weight_lowrank_free"]
+               "iga_weight_lowrank_sep", "iga_weight_lowrank_free", "iga_lr_terms", "iga_tt_kron_apply",
+               "iga_tt_interfaces", "iga_tt_local_apply"]
 MINRES_X0 = 0x100
 
 
@@ -109,6 +110,13 @@ _lib.iga_weight_lowrank_sep.argtypes = [_P, ctypes.POINTER(_Sep), ctypes.POINTER
                                         ctypes.POINTER(ctypes.c_double)]
 _lib.iga_weight_lowrank_free.argtypes = [_P]
 _lib.iga_weight_lowrank_free.restype = None
+_I32P = ctypes.POINTER(ctypes.c_int32)
+_lib.iga_lr_terms.argtypes = [_P, ctypes.c_int32, _I32P, _I32P, _D]
+_lib.iga_tt_kron_apply.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P]
+_lib.iga_tt_interfaces.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
+                                   _P, _P, _P]
+_lib.iga_tt_local_apply.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
+                                    _P, _P]
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -287,6 +295,41 @@ class LowRankOperator:
         tab = ctypes.c_int32(0)
         _check(_lib.iga_lr_export_factor(self._h, d, fid, _dptr(band), ctypes.byref(pat), ctypes.byref(tab)))
         return band, pat.value, tab.value
+
+    # ------------------------------------------------------------------ TT (NEXT-3)
+    def terms(self, part: int) -> Tuple[np.ndarray, np.ndarray]:
+        """The op's Kronecker terms of `part` (0 mass, 1 stiffness): fid [T, 3] (x, y, z factor
+        ids, see export_factor) and coef [T] (iga_lr_terms)."""
+        T = ctypes.c_int32(0)
+        _check(_lib.iga_lr_terms(self._h, int(part), ctypes.byref(T), None, None))
+        fid = np.zeros((T.value, 3), dtype=np.int32)
+        coef = np.zeros(T.value)
+        _check(_lib.iga_lr_terms(self._h, int(part), ctypes.byref(T), fid.ctypes.data_as(_I32P), _dptr(coef)))
+        return fid, coef
+
+    def tt_kron_apply(self, part: int, gz, gy, gx, wz, wy, wx, stream=None):
+        """A v for a TT vector v with device cores gz [mz, R1], gy [R1, my, R2], gx [R2, mx]:
+        per-term cores wz [T, mz, R1] (coefficient folded in), wy [T, R1, my, R2], wx [T, R2, mx]
+        (iga_tt_kron_apply)."""
+        R1, R2 = int(gy.shape[0]), int(gy.shape[2])
+        _check(_lib.iga_tt_kron_apply(self._h, int(part), R1, R2, _tensor_ptr(gz, "gz"), _tensor_ptr(gy, "gy"),
+                                      _tensor_ptr(gx, "gx"), _tensor_ptr(wz, "wz"), _tensor_ptr(wy, "wy"),
+                                      _tensor_ptr(wx, "wx"), _stream_handle(stream)))
+
+    def tt_interfaces(self, part: int, site: int, gz, gy, gx, L, R, stream=None):
+        """Frame interfaces of `site` (0 x, 1 y, 2 z) for every term: L [T, Rl, Rl], R [T, Rr, Rr]
+        (iga_tt_interfaces)."""
+        R1, R2 = int(gy.shape[0]), int(gy.shape[2])
+        _check(_lib.iga_tt_interfaces(self._h, int(part), int(site), R1, R2, _tensor_ptr(gz, "gz"),
+                                      _tensor_ptr(gy, "gy"), _tensor_ptr(gx, "gx"), _tensor_ptr(L, "L"),
+                                      _tensor_ptr(R, "R"), _stream_handle(stream)))
+
+    def tt_local_apply(self, part: int, site: int, L, R, x, y, stream=None):
+        """y = (sum_t c_t L_t (x) A_t^(site) (x) R_t) x for local cores x, y [Rl, m_site, Rr]
+        (iga_tt_local_apply)."""
+        _check(_lib.iga_tt_local_apply(self._h, int(part), int(site), int(x.shape[0]), int(x.shape[2]),
+                                       _tensor_ptr(L, "L"), _tensor_ptr(R, "R"), _tensor_ptr(x, "x"),
+                                       _tensor_ptr(y, "y"), _stream_handle(stream)))
 
     # ------------------------------------------------------------------ device applies
     def apply(self, x, y_mass=None, y_stiff=None, alpha: float = 1.0, gamma: float = 1.0, path: str = "auto",

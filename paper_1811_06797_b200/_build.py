@@ -19,7 +19,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_fused2.cu", "canon_p3.cu",
-           "canon_p4.cu", "kkt.cu", "minres.cu", "prec.cu", "weights.cu"]
+           "canon_p4.cu", "kkt.cu", "minres.cu", "prec.cu", "weights.cu", "tt.cu"]
 
 
 def _newer(src_paths, target):

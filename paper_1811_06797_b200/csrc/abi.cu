@@ -403,6 +403,17 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     }
     std::vector<Term> tm, ts;
     for (auto& t : terms) (t.part == 0 ? tm : ts).push_back(t);
+    // merged term list for the TT functions (NEXT-3): identical (part, factors) terms summed
+    for (const Term& t : terms) {
+        bool merged = false;
+        for (KTerm& u : op->kterms)
+            if (u.part == t.part && u.f[0] == t.f[0] && u.f[1] == t.f[1] && u.f[2] == t.f[2]) {
+                u.c += t.c;
+                merged = true;
+                break;
+            }
+        if (!merged) op->kterms.push_back({t.part, {t.f[0], t.f[1], t.f[2]}, t.c});
+    }
     build_plan(op, terms, false, &op->plan[kPlanBoth]);
     build_plan(op, terms, true, &op->plan[kPlanBothSplit]);
     build_plan(op, tm, false, &op->plan[kPlanMass]);

@@ -89,6 +89,15 @@ struct Plan {
 enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kPlanF2Mass = 4, kPlanF2Stiff = 5, kNumPlans = 6 };
 }  // namespace igalr
 
+namespace igalr {
+// One Kronecker term c * F^z (x) F^y (x) F^x of a part (factor ids per direction x, y, z).
+struct KTerm {
+    int part;
+    int f[3];
+    double c;
+};
+}  // namespace igalr
+
 struct iga_lr_op {
     int n[3], p[3], m[3], nq;
     bool dirichlet;
@@ -98,6 +107,7 @@ struct iga_lr_op {
     igalr::Plan plan[igalr::kNumPlans];
     double min_bytes = 0;
     int device = 0;
+    std::vector<igalr::KTerm> kterms;  // merged term list, r-major (NEXT-3 TT functions)
     // fixup tables of the canonical kernels, per launch shape (built on first use; fused2_impl.cuh)
     struct FixCache {
         long long key[9];

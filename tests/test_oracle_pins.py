@@ -534,3 +534,54 @@ def test_weights3d_annulus_volume_and_constants():
     one = np.ones(P.ndof)
     assert abs(one @ (M @ one) - g.volume) <= 1e-13 * g.volume
     assert np.abs(S @ one).max() <= 1e-13 * abs(S).max()
+
+
+# ------------------------------------------------------------------ TT oracle (NEXT-3)
+def _cores(rng, m, R1, R2):
+    mz, my, mx = m
+    return (rng.standard_normal((mz, R1)), rng.standard_normal((R1, my, R2)), rng.standard_normal((R2, mx)))
+
+
+def test_tt_full_brute_force():
+    rng = np.random.default_rng(1)
+    gz, gy, gx = _cores(rng, (3, 4, 2), 2, 3)
+    v = oracle.tt_full(gz, gy, gx)
+    for iz, iy, ix in [(0, 0, 0), (2, 3, 1), (1, 2, 0)]:
+        ref = sum(gz[iz, a] * gy[a, iy, b] * gx[b, ix] for a in range(2) for b in range(3))
+        assert abs(v[iz, iy, ix] - ref) <= 1e-14
+
+
+@pytest.mark.parametrize("site", [0, 1, 2])
+def test_tt_frame_linearity(site):
+    """Eq. (ttlin): F_{!=d} vec(G_d) is the represented tensor."""
+    rng = np.random.default_rng(2 + site)
+    gz, gy, gx = _cores(rng, (3, 4, 5), 2, 3)
+    F = oracle.tt_frame(gz, gy, gx, site)
+    vec = {0: gx.ravel(), 1: gy.ravel(), 2: gz.ravel()}[site]
+    assert np.allclose(F @ vec, oracle.tt_full(gz, gy, gx).ravel(), atol=1e-13)
+
+
+@pytest.mark.parametrize("site", [0, 1, 2])
+def test_tt_projection_identity_and_symmetry(site):
+    """Orthogonal frames project the identity to the identity (the SVD makes
+    the frame orthogonal); a symmetric operator projects to a symmetric matrix."""
+    rng = np.random.default_rng(7)
+    m = (4, 5, 3)
+    gz, gy, gx = _cores(rng, m, 2, 3)
+    # orthogonalise the cores away from the site: left cores left-orthogonal, right ones right-orthogonal
+    if site in (0, 1):
+        gz = np.linalg.qr(gz)[0]
+    if site == 0:
+        q = np.linalg.qr(gy.reshape(-1, gy.shape[2]))[0]
+        gy = q.reshape(gy.shape)
+    if site in (1, 2):
+        gx = np.linalg.qr(gx.T)[0].T
+    if site == 2:
+        q = np.linalg.qr(gy.reshape(gy.shape[0], -1).T)[0].T
+        gy = q.reshape(gy.shape)
+    N = m[0] * m[1] * m[2]
+    P = oracle.tt_project(np.eye(N), gz, gy, gx, site)
+    assert np.allclose(P, np.eye(P.shape[0]), atol=1e-12)
+    B = rng.standard_normal((N, N))
+    Ps = oracle.tt_project(B + B.T, gz, gy, gx, site)
+    assert np.allclose(Ps, Ps.T, atol=1e-12)
