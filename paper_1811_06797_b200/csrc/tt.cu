@@ -113,22 +113,12 @@ __global__ void k_tt_left(const double* __restrict__ S, const double* __restrict
     }
 }
 
-// y[r][i][s] = sum_t c_t sum_{r'} L[t][r][r'] Bt[t][r'][i][s]
-__global__ void k_tt_local_final(const double* __restrict__ L, const double* __restrict__ Bt, const TermTab tab,
-                                 double* __restrict__ y, int Rl, int m, int Rr) {
-    const long long per = (long long)Rl * m * Rr;
+// y[id] = sum_t c_t Z[t][id]  (terms summed in order)
+__global__ void k_tt_sum_terms(const double* __restrict__ Z, const TermTab tab, double* __restrict__ y, long long per) {
     for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < per;
          id += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(id / ((long long)m * Rr));
-        const long long is = id - (long long)r * m * Rr;
         double s = 0.0;
-        for (int t = 0; t < tab.T; ++t) {
-            const double* lr = L + ((long long)t * Rl + r) * Rl;
-            const double* b = Bt + t * per + is;
-            double u = 0.0;
-            for (int q = 0; q < Rl; ++q) u = fma(lr[q], b[(long long)q * m * Rr], u);
-            s = fma(tab.coef[t], u, s);
-        }
+        for (int t = 0; t < tab.T; ++t) s = fma(tab.coef[t], Z[t * per + id], s);
         y[id] = s;
     }
 }
@@ -323,8 +313,13 @@ iga_status iga_tt_local_apply(const iga_lr_op* op, int32_t part, int32_t site, i
         e = cudaGetLastError();
         // b[t] = A_t^(d) a[t] along the physical index
         if (!e) e = mode(op, site, tab, false, a, (long long)per, b, Rl, Rr, st);
+        // c[t][r][i][s] = sum_{r'} L_t[r][r'] b[t][r'][i][s] (into a), then y = sum_t c_t c[t]
         if (!e) {
-            k_tt_local_final<<<grid_for((long long)per), 256, 0, st>>>(L, b, tab, y, Rl, m, Rr);
+            k_tt_left<<<grid_for((long long)per * T), 256, 0, st>>>(L, b, a, T, Rl, m, Rr);
+            e = cudaGetLastError();
+        }
+        if (!e) {
+            k_tt_sum_terms<<<grid_for((long long)per), 256, 0, st>>>(a, tab, y, (long long)per);
             e = cudaGetLastError();
         }
     }
