@@ -456,6 +456,9 @@ void iga_lr_destroy(iga_lr_op* op) {
         if (op->plan[k].d_ztab) cudaFree(op->plan[k].d_ztab);
     }
     if (op->side) cudaStreamDestroy(op->side);
+    if (op->host_sh) cudaStreamDestroy(op->host_sh);
+    if (op->host_sd) cudaStreamDestroy(op->host_sd);
+    for (cudaEvent_t x : op->host_ev) cudaEventDestroy(x);
     for (auto& c : op->fix_cache) {
         if (c.d_tab) cudaFree(c.d_tab);
     }
@@ -663,6 +666,8 @@ iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* 
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)op->m[0] * op->m[1] * op->m[2];
     const size_t tot = N * batch;
+    // one host pipeline per op at a time: its copy streams and events are cached in the op
+    std::lock_guard<std::mutex> pipe_lock(op->host_mu);
     double *d_in = nullptr, *d_out = nullptr;
     const bool same = y_mass_host && y_mass_host == y_stiff_host;
     int nout = same ? 1 : (y_mass_host ? 1 : 0) + (y_stiff_host ? 1 : 0);
@@ -675,22 +680,46 @@ iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* 
     double* dm = y_mass_host ? d_out : nullptr;
     double* ds = y_stiff_host ? (same ? d_out : d_out + (y_mass_host ? tot : 0)) : nullptr;
     const int nchunk = batch;
-    cudaStream_t sh = nullptr, sd = nullptr;
-    std::vector<cudaEvent_t> ev(2 * nchunk + 2, nullptr);
+    // copy streams (H2D, D2H) and 3 events per chunk + 2, created once per op
+    if (!op->host_sh) e = cudaStreamCreateWithFlags(&op->host_sh, cudaStreamNonBlocking);
+    if (!e && !op->host_sd) e = cudaStreamCreateWithFlags(&op->host_sd, cudaStreamNonBlocking);
+    const size_t nev = 3 * (size_t)nchunk + 2;
+    while (!e && op->host_ev.size() < nev) {
+        cudaEvent_t x = nullptr;
+        e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        if (!e) op->host_ev.push_back(x);
+    }
+    cudaStream_t sh = op->host_sh, sd = op->host_sd;
+    const std::vector<cudaEvent_t>& ev = op->host_ev;
     iga_status s = IGA_OK;
-    e = cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking);
-    if (!e) e = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
-    for (size_t k = 0; k < ev.size() && !e; ++k) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
     if (!e) e = cudaEventRecord(ev[0], st);  // buffers allocated
     if (!e) e = cudaStreamWaitEvent(sh, ev[0], 0);
     if (!e) e = cudaStreamWaitEvent(sd, ev[0], 0);
+    // per vector: H2D (sh) -> mass part (st) -> D2H of y_M (sd) overlapping the stiffness part
+    // (st) -> D2H of y_S (sd); the D2H stream is the bottleneck (PCIe), so the first y_M leaves
+    // while the first stiffness part still runs
+    const bool split = y_mass_host && y_stiff_host && !same;
     for (int c = 0; c < nchunk && !e && !s; ++c) {
         const size_t off = (size_t)c * N;
-        cudaEvent_t ein = ev[2 + 2 * c], eout = ev[3 + 2 * c];
+        cudaEvent_t ein = ev[2 + 3 * c], em = ev[3 + 3 * c], eout = ev[4 + 3 * c];
         e = cudaMemcpyAsync(d_in + off, x_host + off, sizeof(double) * N, cudaMemcpyHostToDevice, sh);
         if (!e) e = cudaEventRecord(ein, sh);
         if (!e) e = cudaStreamWaitEvent(st, ein, 0);
         if (e) break;
+        if (split) {
+            s = iga_lr_apply(op, d_in + off, dm + off, nullptr, alpha, gamma, 1, flags, stream);
+            if (s) break;
+            e = cudaEventRecord(em, st);
+            if (!e) e = cudaStreamWaitEvent(sd, em, 0);
+            if (!e) e = cudaMemcpyAsync(y_mass_host + off, dm + off, sizeof(double) * N, cudaMemcpyDeviceToHost, sd);
+            if (e) break;
+            s = iga_lr_apply(op, d_in + off, nullptr, ds + off, alpha, gamma, 1, flags, stream);
+            if (s) break;
+            e = cudaEventRecord(eout, st);
+            if (!e) e = cudaStreamWaitEvent(sd, eout, 0);
+            if (!e) e = cudaMemcpyAsync(y_stiff_host + off, ds + off, sizeof(double) * N, cudaMemcpyDeviceToHost, sd);
+            continue;
+        }
         s = iga_lr_apply(op, d_in + off, dm ? dm + off : nullptr, ds ? ds + off : nullptr, alpha, gamma, 1, flags,
                          stream);
         if (s) break;
@@ -702,15 +731,11 @@ iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* 
             e = cudaMemcpyAsync(y_stiff_host + off, ds + off, sizeof(double) * N, cudaMemcpyDeviceToHost, sd);
     }
     // the caller's stream waits for the last D2H before the buffers are released
-    cudaError_t e3 = cudaEventRecord(ev[1], sd);
+    cudaError_t e3 = ev.size() > 1 ? cudaEventRecord(ev[1], sd) : cudaErrorInvalidValue;
     if (!e3) e3 = cudaStreamWaitEvent(st, ev[1], 0);
     cudaFreeAsync(d_in, st);
     cudaFreeAsync(d_out, st);
     cudaError_t e2 = cudaStreamSynchronize(st);
-    if (sh) cudaStreamDestroy(sh);
-    if (sd) cudaStreamDestroy(sd);
-    for (cudaEvent_t x : ev)
-        if (x) cudaEventDestroy(x);
     if (s) return s;
     if (e) return cuda_error(e, "host apply pipeline");
     if (e3) return cuda_error(e3, "host apply pipeline");

@@ -119,6 +119,10 @@ struct iga_lr_op {
     // side stream for running the mass part beside the stiffness part on small grids (lazily
     // created under fix_mu; abi.cu run_f2)
     mutable cudaStream_t side = nullptr;
+    // host-buffer pipeline (iga_lr_apply_host): copy streams and events, created on first use
+    mutable std::mutex host_mu;
+    mutable cudaStream_t host_sh = nullptr, host_sd = nullptr;
+    mutable std::vector<cudaEvent_t> host_ev;
 };
 
 namespace igalr {
