@@ -665,6 +665,9 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     // the group's x-coefficients, so rounds are separated by a group barrier (named barrier
     // 1 + grp) and only the first round of a plane (new plane buffer) by a CTA barrier.
     constexpr bool GSYNC = gsync_path<P, TMA, YRES>();
+    // GSYNC plane staging: lane 0 of every warp issues a share of the row copies (DIST) or
+    // thread 0 issues all of them
+    constexpr bool DIST = !(P == 3 && QX == 4);
     const int grp = GSYNC ? cg : 0;
     constexpr int GTHREADS = GSYNC ? 32 * WPQ * (4 / QX) : NW * WPQ * 32;
     const bool gprod = GSYNC ? (warp == grp && lane == 0) : (threadIdx.x == 0);  // x-copy issuer
@@ -735,23 +738,43 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             for (int i = 0; i < LW; ++i) ring_st<BW, TIGHTR>(tbase + i * RS::COLS, zero);
         }
 
+        // GSYNC: the byte count of a plane's copies, registered by thread 0 before they are issued
+        auto stage_plane_expect = [&](int buf) {
+            if (threadIdx.x == 0) {
+                const int cbase = x0 - P - PADL;
+                const int cs = max(cbase, 0);
+                const int ce = min((min(x0 + TX + P, a.mx) + 1) & ~1, a.mx);
+                const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
+                const uint32_t rb = (uint32_t)((ce - cs) * sizeof(double));
+                const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
+                mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
+            }
+        };
         auto stage_plane = [&](int zp, int buf) {
             if constexpr (GSYNC) {
-                // one thread: the in-range part of every tile row (widened to an even, 16-byte
-                // aligned column range) and the plane's z record, completing on pbar[buf]
-                if (threadIdx.x == 0) {
+                // the in-range part of every tile row (widened to an even, 16-byte aligned column
+                // range) and the plane's z record, completing on pbar[buf].  Thread 0 registers the
+                // byte count first (stage_plane_expect, before the CTA barrier); lane 0 of every
+                // warp then issues its share of the row copies (one thread issuing all HY rows
+                // delayed warp 0 by a few hundred instructions per plane)
+                // (DIST: measured per tile shape; the p = 3, 128-wide sweep ran 1.5 % slower with
+                // it, so that shape keeps one issuing thread)
+                if (DIST ? lane == 0 : threadIdx.x == 0) {
+                    if (!DIST) stage_plane_expect(buf);
                     const int cbase = x0 - P - PADL;
                     const int cs = max(cbase, 0);
                     const int ce = min((min(x0 + TX + P, a.mx) + 1) & ~1, a.mx);
                     const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
                     const uint32_t rb = (uint32_t)((ce - cs) * sizeof(double));
-                    const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
-                    mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
                     double* dstp = vin + buf * VSZ + (cs - cbase);
                     const double* srcp = a.src + vbs + (long long)zp * plane + cs;
-                    for (int r = rlo; r < rhi; ++r)
+                    for (int r = rlo + (DIST ? warp : 0); r < rhi; r += (DIST ? NW * WPQ : 1))
                         bulk_g2s(dstp + r * HXP, srcp + (long long)(y0 - P + r) * a.mx, rb, &pbar[buf]);
-                    bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes, &pbar[buf]);
+                    if (!DIST || warp == NW * WPQ - 1) {
+                        const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
+                        bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes,
+                                 &pbar[buf]);
+                    }
                 }
                 return;
             }
@@ -825,6 +848,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             }
         };
 
+        if constexpr (GSYNC && DIST) {
+            stage_plane_expect(0);
+            __syncthreads();  // the expected byte count is registered before any copy completes
+        }
         stage_plane(za, 0);
         stage_xc(0, 0);
         cp_commit();
@@ -836,6 +863,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     tm_wait_st();
                     if (r == 0) {  // new plane buffer: CTA barrier, then request plane z'+1
                         cp_wait<0>();  // (resident y-coefficients at a segment start)
+                        if (DIST && zp + 1 < zb) stage_plane_expect(pbuf ^ 1);
                         __syncthreads();
                         if (zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
                         mbar_wait(&pbar[pbuf], (pph >> pbuf) & 1);
