@@ -27,6 +27,12 @@ What it computes (each function cites the passage it follows):
 * ``greville``, ``tt_svd``, ``weight_lowrank``  NEXT-2: samples at Greville points -> TT-SVD ->
                           univariate collocation solves -> canonical terms tabulated at nodes
                           (PAPER.md:177-265).
+* ``Problem.weights3d``   NEXT-4: general (non-separable) omega and Q given at every 3D quadrature
+                          point, e.g. a geometry's |det grad G| and (grad G^T grad G)^-1 |det grad G|
+                          (PAPER.md:127-133), in the same assembly of Eqs. (massMatrix)/(stiffnessMatrix).
+* ``tt_full``, ``tt_frame``, ``tt_project``  NEXT-3: the TT tensor of Eq. (tt),
+                          the frame matrix of Eq. (frame) and F^T A F of
+                          Eq. (KKT_red), dense, desk sizes.
 
 Parity pins: tests/test_oracle_pins.py (P1-P12 of SURVEY.md §8(c)).
 Every function here is pinned; none is "parity unpinned".
