@@ -1046,18 +1046,45 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     });
 #pragma unroll
                     for (int i = 0; i < LW; ++i) tm_st1(tbase + i * RS::COLS + 2 * jret, 0.0);
+                    // (measured per shape: the p = 4 mass kernel is 2.7 % faster with per-row branches)
+                    constexpr bool SPLITSTORE = !(P >= 4 && !std::is_same<S, ShapeStiffA>::value);
+                    if constexpr (SPLITSTORE) {
+                        // stores: the plane-uniform cases (complete / partial, accumulate) are split
+                        // outside the row loop, so each row is one predicated store (no per-row branches)
+                        const int nrow = min(LW, a.my - (y0 + row0));  // rows of this warp inside the mesh
+                        const bool colok = gx < a.mx;
+                        if (ret_complete) {
+                            double* drow = a.dst + vbd + (long long)zret * plane + (long long)(y0 + row0) * a.mx + gx;
+                            if (a.accumulate) {
 #pragma unroll
-                    for (int i = 0; i < LW; ++i) {
-                        const double val = rv[i];
-                        const int gy = y0 + row0 + i;
-                        if (gy < a.my && gx < a.mx) {
-                            if (ret_complete) {
-                                const long long o = vbd + (long long)zret * plane + (long long)gy * a.mx + gx;
-                                a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                for (int i = 0; i < LW; ++i)
+                                    if (colok && i < nrow) drow[(long long)i * a.mx] += a.scale * rv[i];
                             } else {
-                                const int slot = partial_slot(zret, za, zb, P);
-                                a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
-                                    a.scale * val;
+#pragma unroll
+                                for (int i = 0; i < LW; ++i)
+                                    if (colok && i < nrow) drow[(long long)i * a.mx] = a.scale * rv[i];
+                            }
+                        } else {
+                            const int slot = partial_slot(zret, za, zb, P);
+                            double* srow = a.scratch + ((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0) * TX + cx;
+#pragma unroll
+                            for (int i = 0; i < LW; ++i)
+                                if (colok && i < nrow) srow[(size_t)i * TX] = a.scale * rv[i];
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) {
+                            const double val = rv[i];
+                            const int gy = y0 + row0 + i;
+                            if (gy < a.my && gx < a.mx) {
+                                if (ret_complete) {
+                                    const long long o = vbd + (long long)zret * plane + (long long)gy * a.mx + gx;
+                                    a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                } else {
+                                    const int slot = partial_slot(zret, za, zb, P);
+                                    a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
+                                        a.scale * val;
+                                }
                             }
                         }
                     }
