@@ -155,12 +155,157 @@ __global__ void __launch_bounds__(256) k_mode_lines(const double* __restrict__ A
     }
 }
 
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) form of the same dense mode product for n <= 64:
+// the fast-diagonalisation transforms are dense n x n contractions, the one place on this path
+// where a dense tile is not mostly padding (n = 46: 92 % of each 48 x 48 tile is useful).
+// A CTA takes a 64-column tile X[j][c] (slab: columns of one o; LINES: 64 contiguous lines,
+// staged transposed), out = A X as 8x8 tiles: warp w owns columns 8w..8w+7 and every 8-row
+// tile, accumulating over k-steps of 4.  Fragments (PTX m8n8k4 .f64): a = A[l/4][l%4],
+// b = X[l%4][l/4], d = D[l/4][2(l%4) + {0,1}] for lane l.
+constexpr int kMmaC = 64;
+template <bool LINES>
+__global__ void __launch_bounds__(256, 3) k_mode_mma(const double* __restrict__ A, const double* __restrict__ in,
+                                                  double* __restrict__ out, long long outer, int n, long long inner) {
+    extern __shared__ double sm[];
+    const int NM = (n + 7) & ~7, KN = (n + 3) & ~3;
+    const int XP = kMmaC + 8;               // X pitch (== 8 mod 16 doubles)
+    double* As = sm;                        // [NM/8][KN/4][32] fragment order
+    double* Xs = As + NM * KN;              // [KN][XP], columns swizzled (xs below)
+    double* Os = Xs + KN * XP;              // LINES: [kMmaC][n + 1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // X tile index with the column XOR-swizzled by (row/2)%8: the staging stores (16 consecutive
+    // rows of one column for LINES, consecutive columns for slabs) and the B-fragment loads
+    // (rows k..k+3 x 8 columns) each touch all 16 eight-byte banks once per wavefront
+    auto xs = [&](int j, int c) { return j * XP + (c ^ ((j >> 1) & 7)); };
+    // A in fragment order: As[(m * (KN/4) + k) * 32 + l] = A[8m + l/4][4k + l%4], so a warp's
+    // fragment load is 32 consecutive doubles (no bank conflicts)
+    const int KS = KN >> 2;
+    for (int t = threadIdx.x; t < NM * KN; t += blockDim.x) {
+        const int l = t & 31, mk = t >> 5;
+        const int m = mk / KS, k = mk - m * KS;
+        const int i = m * 8 + (l >> 2), j = k * 4 + (l & 3);
+        As[t] = (i < n && j < n) ? A[i * n + j] : 0.0;
+    }
+    const long long nchunk = LINES ? (outer + kMmaC - 1) / kMmaC : (inner + kMmaC - 1) / kMmaC;
+    const long long nblk = LINES ? nchunk : outer * nchunk;
+    // tile coordinates: (o, c0, cw)
+    auto tile = [&](long long blk, long long& o, long long& c0, int& cw) {
+        if (LINES) {
+            o = 0;
+            c0 = blk * kMmaC;
+            cw = (int)min((long long)kMmaC, outer - c0);
+        } else {
+            o = blk / nchunk;
+            c0 = (blk - o * nchunk) * kMmaC;
+            cw = (int)min((long long)kMmaC, inner - c0);
+        }
+    };
+    // staging: all of a thread's loads (<= 16) are issued before its shared-memory stores
+    constexpr int kPer = (64 * kMmaC) / 256;
+    auto load = [&](long long blk, double* v) {
+        long long o, c0;
+        int cw;
+        tile(blk, o, c0, cw);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int t = threadIdx.x + q * 256;
+            if (LINES) {
+                const int ll = t / n, j = t - ll * n;
+                v[q] = (t < kMmaC * n && ll < cw) ? __ldg(in + (c0 + ll) * n + j) : 0.0;
+            } else {
+                const int j = t / kMmaC, cc = t - j * kMmaC;
+                v[q] = (t < n * kMmaC && cc < cw) ? __ldg(in + (o * n + j) * inner + c0 + cc) : 0.0;
+            }
+        }
+    };
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        long long o, c0;
+        int cw;
+        tile(blk, o, c0, cw);
+        double v[kPer];
+        load(blk, v);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int t = threadIdx.x + q * 256;
+            if (LINES) {
+                const int ll = t / n, j = t - ll * n;
+                if (t < kMmaC * n) Xs[xs(j, ll)] = v[q];
+            } else {
+                const int j = t / kMmaC, cc = t - j * kMmaC;
+                if (t < n * kMmaC) Xs[xs(j, cc)] = v[q];
+            }
+        }
+        for (int t = threadIdx.x; t < (KN - n) * kMmaC; t += blockDim.x)  // zero K padding rows
+            Xs[xs(n + t / kMmaC, t % kMmaC)] = 0.0;
+        __syncthreads();
+        double acc[8][2];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[m][0] = acc[m][1] = 0.0;
+        const int nm = NM >> 3;
+        for (int k0 = 0; k0 < KN; k0 += 4) {
+            const double b = Xs[xs(k0 + (lane & 3), warp * 8 + (lane >> 2))];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                if (m < nm) {
+                    const double a = As[(m * KS + (k0 >> 2)) * 32 + lane];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(acc[m][0]), "+d"(acc[m][1])
+                                 : "d"(a), "d"(b));
+                }
+            }
+        }
+        const int col = warp * 8 + 2 * (lane & 3);
+        if (LINES) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int i = m * 8 + (lane >> 2);
+                if (m < nm && i < n) {
+                    Os[col * (n + 1) + i] = acc[m][0];
+                    Os[(col + 1) * (n + 1) + i] = acc[m][1];
+                }
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < cw * n; t += blockDim.x) {  // contiguous global writes
+                const int ll = t / n, i = t - ll * n;
+                out[(c0 + ll) * n + i] = Os[ll * (n + 1) + i];
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int i = m * 8 + (lane >> 2);
+                if (m < nm && i < n) {
+                    double* dst = out + (o * n + i) * inner + c0 + col;
+                    if (col < cw) dst[0] = acc[m][0];
+                    if (col + 1 < cw) dst[1] = acc[m][1];
+                }
+            }
+        }
+    }
+}
+
 // out = A x_d in along the middle index of [outer][n][inner]
 void mode_product(const double* A, const double* in, double* out, long long outer, int n, long long inner,
                   cudaStream_t st) {
     const long long tot = outer * n * inner;
     if (n > 8 * kSlabRows) {
         k_mode<<<grid_of(tot), 256, 0, st>>>(A, in, out, outer, n, inner);
+        return;
+    }
+    {
+        // DMMA path (n <= 64)
+        const int NM = (n + 7) & ~7, KN = (n + 3) & ~3;
+        const size_t sm = sizeof(double) * ((size_t)NM * KN + (size_t)KN * (kMmaC + 8) +
+                                            (inner == 1 ? (size_t)kMmaC * (n + 1) : 0));
+        const long long nblk = inner == 1 ? (outer + kMmaC - 1) / kMmaC : outer * ((inner + kMmaC - 1) / kMmaC);
+        const int grid = (int)std::min(nblk, 148LL * 8);
+        if (inner == 1) {
+            cudaFuncSetAttribute(k_mode_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_mode_mma<true><<<grid, 256, sm, st>>>(A, in, out, outer, n, inner);
+        } else {
+            cudaFuncSetAttribute(k_mode_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_mode_mma<false><<<grid, 256, sm, st>>>(A, in, out, outer, n, inner);
+        }
         return;
     }
     if (inner == 1) {
@@ -204,16 +349,15 @@ __global__ void k_prec_point(double* __restrict__ t, int n_t, int mx, int my, in
     }
 }
 
-// three mode products of W (trans = false) or W' (trans = true) on B vectors: in -> out (tmp used)
-void apply_W(const iga_kkt_prec* P, bool trans, long long B, const double* in, double* out, double* tmp,
+// three mode products of W (trans = false) or W' (trans = true) on B vectors, without copies:
+// in -> mid (x), mid -> res (y), res -> mid (z); the result lands in `mid`, `res` is scratch
+void apply_W(const iga_kkt_prec* P, bool trans, long long B, const double* in, double* mid, double* res,
              cudaStream_t st) {
     const long long mx = P->m[0], my = P->m[1], mz = P->m[2];
     const double* const* A = trans ? P->dAt : P->dA;
-    const long long tot = B * mx * my * mz;
-    mode_product(A[0], in, tmp, B * mz * my, (int)mx, 1, st);
-    mode_product(A[1], tmp, out, B * mz, (int)my, mx, st);
-    mode_product(A[2], out, tmp, B, (int)mz, my * mx, st);
-    cudaMemcpyAsync(out, tmp, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st);
+    mode_product(A[0], in, mid, B * mz * my, (int)mx, 1, st);
+    mode_product(A[1], mid, res, B * mz, (int)my, mx, st);
+    mode_product(A[2], res, mid, B, (int)mz, my * mx, st);
 }
 
 }  // namespace
@@ -221,12 +365,18 @@ void apply_W(const iga_kkt_prec* P, bool trans, long long B, const double* in, d
 iga_status kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, double* tmp, cudaStream_t st) {
     const long long N = (long long)P->m[0] * P->m[1] * P->m[2];
     const long long B = 3LL * P->n_t;
-    apply_W(P, true, B, in, out, tmp, st);  // out = W' in
-    k_prec_point<<<grid_of(N), 256, 0, st>>>(out, P->n_t, P->m[0], P->m[1], P->m[2], P->dlam[0], P->dlam[1],
+    apply_W(P, true, B, in, tmp, out, st);  // tmp = W' in   (out as scratch)
+    k_prec_point<<<grid_of(N), 256, 0, st>>>(tmp, P->n_t, P->m[0], P->m[1], P->m[2], P->dlam[0], P->dlam[1],
                                              P->dlam[2], 1.0 / (P->tau * P->mbar),
                                              1.0 / (P->tau * P->beta * P->mbar), (1.0 + P->g) * P->mbar,
                                              P->tau * P->sbar, P->mbar, P->tau);
-    apply_W(P, false, B, out, out, tmp, st);  // out = W out
+    // W tmp: tmp -> out (x), out -> tmp (y), tmp -> out (z); no copies
+    {
+        const long long mx = P->m[0], my = P->m[1], mz = P->m[2];
+        mode_product(P->dA[0], tmp, out, B * mz * my, (int)mx, 1, st);
+        mode_product(P->dA[1], out, tmp, B * mz, (int)my, mx, st);
+        mode_product(P->dA[2], tmp, out, B, (int)mz, my * mx, st);
+    }
     cudaError_t e = cudaGetLastError();
     if (e) return cuda_error(e, "kkt preconditioner");
     return IGA_OK;
