@@ -99,7 +99,10 @@ def dist_setup(backend: str = "nccl"):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
+        if backend == "nccl":
+            torch.cuda.set_device(local)  # before NCCL init: one GPU per rank
         if not dist.is_initialized():
             dist.init_process_group(backend)
     return ws, rank, local
