@@ -176,6 +176,24 @@ def test_full_size_sampled_rows(env, cfgname):
         assert rel(gm, rm) <= TOL and rel(gs, rs) <= TOL
 
 
+@pytest.mark.parametrize("minlen", [1, 2, 3, 5])
+def test_fixup_table_many_contributors(env, minlen, monkeypatch):
+    """Persistent-CTA ranges of `minlen` planes (IGALR_MINLEN, an experiment knob) give output
+    planes with up to 2P+1 contributors in the table-driven fixup; every setting matches the
+    oracle (the summation order, not the result, depends on the split)."""
+    torch, igalr, workloads = env
+    monkeypatch.setenv("IGALR_MINLEN", str(minlen))
+    cfg = synth.scaled(synth.CONFIGS["c3"], 21, batch=2)
+    knots, w, x = synth.draw_problem(cfg)
+    op = workloads.build_operator(cfg, w)
+    yM, yS = gpu_apply(env, op, x, "auto")
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    for b in range(cfg.batch):
+        assert rel(yM[b].ravel(), oracle.spmv(M, x[b])) <= TOL
+        assert rel(yS[b].ravel(), oracle.spmv(S, x[b])) <= TOL
+
+
 @pytest.mark.parametrize("n,batch", [(104, 1), (101, 2)])
 def test_p4_26row_tiles_sampled_rows(env, n, batch):
     """p = 4 meshes whose y extent tiles best in 26-row tiles (LW 13, the 9-double TMEM ring):
