@@ -24,6 +24,10 @@
  *     iga_lr_assemble_factors (it waits for its own uploads) and the *_host entry points.
  *   - Thread safety: an iga_lr_op is immutable after assembly; concurrent applies on
  *     different streams are allowed (scratch memory is stream-ordered, cudaMallocAsync).
+ *     Internally the op caches, behind a mutex: the fixup tables of its launch shapes (built
+ *     on first use with one small H2D copy), a side stream on which small meshes run the mass
+ *     part beside the stiffness part (event fork/join on the caller's stream), and the copy
+ *     streams of iga_lr_apply_host (host-buffer calls on one op run one at a time).
  */
 #ifndef IGA_LR_H
 #define IGA_LR_H
