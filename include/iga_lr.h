@@ -125,7 +125,11 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
    with calM = I_nt (x) M, calK = I_nt (x) tau S + C (x) M, C = bidiagonal (1 on the
    diagonal, -1 below).  in/out: DEVICE fp64 [3][n_t][nz][ny][nx], blocks
    (y, u, lambda).  Needs an op with mass and stiffness (else IGA_ESTATE);
-   tau > 0, beta > 0, n_t >= 1 (else IGA_EINVAL).  in and out must not alias. */
+   tau > 0, beta > 0, n_t >= 1 (else IGA_EINVAL).  in and out must not alias.
+   calK^T carries S^T (PAPER.md:306 writes the y-row as lambda_k (M + tau K)): when the op was
+   assembled with q[k*3+l] and q[l*3+k] that differ (in R, coefficients or tables), S is not
+   symmetric and the op holds a second plan for S^T (block (k,l) of S^T = weight q_kl with the
+   derivative patterns of block (l,k)), so the KKT matrix stays symmetric for MINRES. */
 iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in,
                          double* out, uint32_t flags, void* stream);
 

@@ -277,47 +277,73 @@ def apply_rows(P: Problem, x: np.ndarray, rows: np.ndarray, mass: bool = True, s
 
 
 # ----------------------------------------------------------------------------------- KKT
-def kkt_apply(applyM, applyS, X: np.ndarray, tau: float, beta: float) -> np.ndarray:
+def kkt_apply(applyM, applyS, applyST, X: np.ndarray, tau: float, beta: float) -> np.ndarray:
     """Eq. (KKTSystem) PAPER.md:313-319 applied to X = [y, u, lam], each [n_t, N].
 
     Written as the paper's gradient rows, k = 1..n_t, with
     y_0 = 0 and lambda_{n_t+1} = 0 (reading G9: tau kept as in
     PAPER.md:291,298,308):
-      r_y[k]   = tau M y_k - M lam_{k+1} + M lam_k + tau K lam_k
+      r_y[k]   = tau M y_k - M lam_{k+1} + M lam_k + tau K^T lam_k
       r_u[k]   = tau beta M u_k - tau M lam_k
       r_lam[k] = M y_k - M y_{k-1} + tau K y_k - tau M u_k
-    applyM / applyS map one [N] vector to M v / K v (oracle routes)."""
+    PAPER.md:306 writes the y-row as the row vector lambda_k (M + tau K), i.e. (M + tau K)^T
+    lambda_k, and Eq. (KKTSystem) puts calK^T in the first block row: K^T, not K (the two
+    differ when q_kl != q_lk, which the paper allows: every q_kl is approximated on its own,
+    PAPER.md:202-206).  M is symmetric by Eq. (massMatrix).
+    applyM / applyS / applyST map one [N] vector to M v / K v / K^T v (oracle routes)."""
     y, u, lam = X[0], X[1], X[2]
     nt = y.shape[0]
     My = [applyM(y[k]) for k in range(nt)]
     Mu = [applyM(u[k]) for k in range(nt)]
     Ml = [applyM(lam[k]) for k in range(nt)]
     Sy = [applyS(y[k]) for k in range(nt)]
-    Sl = [applyS(lam[k]) for k in range(nt)]
+    STl = [applyST(lam[k]) for k in range(nt)]
     out = np.zeros_like(X)
     for k in range(nt):
         Ml_next = Ml[k + 1] if k + 1 < nt else 0.0
         My_prev = My[k - 1] if k >= 1 else 0.0
-        out[0, k] = tau * My[k] - Ml_next + Ml[k] + tau * Sl[k]
+        out[0, k] = tau * My[k] - Ml_next + Ml[k] + tau * STl[k]
         out[1, k] = tau * beta * Mu[k] - tau * Ml[k]
         out[2, k] = My[k] - My_prev + tau * Sy[k] - tau * Mu[k]
     return out
 
 
 def kkt_apply_csr(M, S, X: np.ndarray, tau: float, beta: float) -> np.ndarray:
+    """kkt_apply with the CSR routes: M v, S v and S^T v (the transpose of the assembled CSR
+    matrix, scipy.sparse, then the same naive SpMV)."""
     shp = X.shape
     Xf = X.reshape(3, shp[1], -1)
-    out = kkt_apply(lambda v: spmv(M, v), lambda v: spmv(S, v), Xf, tau, beta)
+    ST = S.T.tocsr()
+    out = kkt_apply(lambda v: spmv(M, v), lambda v: spmv(S, v), lambda v: spmv(ST, v), Xf, tau, beta)
     return out.reshape(shp)
+
+
+def transpose_problem(P: Problem) -> Problem:
+    """The problem whose stiffness matrix is K^T: every block q_kl replaced by q_lk.
+    By Eq. (stiffnessMatrix), (K^T)_ij = K_ji = sum_kl int q_kl d_l beta_j
+    d_k beta_i = sum_kl int q_lk d_l beta_i d_k beta_j, i.e. the same definition with Q^T.
+    The mass part is unchanged (M is symmetric)."""
+    qs = P.q_terms
+    qT = None if qs is None else [qs[l * 3 + k] for k in range(3) for l in range(3)]
+    w3 = None
+    if P.weights3d is not None:
+        w3 = np.array(P.weights3d, copy=True)
+        for k in range(3):
+            for l in range(3):
+                w3[1 + k * 3 + l] = P.weights3d[1 + l * 3 + k]
+    return Problem(knots=P.knots, p=P.p, nq=P.nq, mass_terms=P.mass_terms, q_terms=qT, dirichlet=P.dirichlet,
+                   weights3d=w3)
 
 
 def kkt_rows(P: Problem, X: np.ndarray, tau: float, beta: float, steps: Sequence[int],
              rows: np.ndarray) -> np.ndarray:
     """Sampled KKT outputs: out[blk, j, i] for time steps `steps` (0-based) and spatial
-    rows `rows`, via the same three paper rows with row-restricted applies."""
+    rows `rows`, via the same three paper rows with row-restricted applies (K^T v from the
+    transposed problem, transpose_problem)."""
     nt = X.shape[1]
     Xf = X.reshape(3, nt, -1)
     res = np.zeros((3, len(steps), len(rows)))
+    PT = transpose_problem(P)
 
     def M_(v):
         return apply_rows(P, v, rows, mass=True, stiff=False)[0]
@@ -325,13 +351,16 @@ def kkt_rows(P: Problem, X: np.ndarray, tau: float, beta: float, steps: Sequence
     def S_(v):
         return apply_rows(P, v, rows, mass=False, stiff=True)[1]
 
+    def ST_(v):
+        return apply_rows(PT, v, rows, mass=False, stiff=True)[1]
+
     for j, k in enumerate(steps):
         y, u, lam = Xf[0], Xf[1], Xf[2]
         My = M_(y[k]); Mu = M_(u[k]); Ml = M_(lam[k])
         Ml_next = M_(lam[k + 1]) if k + 1 < nt else 0.0
         My_prev = M_(y[k - 1]) if k >= 1 else 0.0
-        Sy = S_(y[k]); Sl = S_(lam[k])
-        res[0, j] = tau * My - Ml_next + Ml + tau * Sl
+        Sy = S_(y[k]); STl = ST_(lam[k])
+        res[0, j] = tau * My - Ml_next + Ml + tau * STl
         res[1, j] = tau * beta * Mu - tau * Ml
         res[2, j] = My - My_prev + tau * Sy - tau * Mu
     return res
@@ -423,7 +452,7 @@ def kkt_prec_dense(P: "Problem", M, S, n_t: int, tau: float, beta: float, exact:
     the unit-weight univariate Grams (gram_1d with amp = 0, Eq. (massMatrix1D) PAPER.md:192-196;
     patterns (0,0) and (1,1)), Dirichlet-sliced like the problem; mbar = v1' M v1 / v1' M0 v1 and
     sbar = v1' S v1 / v1' S0 v1 for v1 = e1z (x) e1y (x) e1x, e1d the eigenvector of the smallest
-    eigenvalue of K0d v = lam M0d v (scipy.linalg.eigh).  exact=True uses M, S themselves
+    positive eigenvalue of K0d v = lam M0d v (scipy.linalg.eigh).  exact=True uses M, S themselves
     (Mh = M, Sh0 = S: the ideal matching preconditioner).  Returns (P, mbar, sbar, lam per dir)."""
     import scipy.linalg as sla
     M0d, K0d, e1, lams = [], [], [], []
@@ -436,7 +465,10 @@ def kkt_prec_dense(P: "Problem", M, S, n_t: int, tau: float, beta: float, exact:
         lam, V = sla.eigh(G1, G0)
         M0d.append(G0)
         K0d.append(G1)
-        e1.append(V[:, int(np.argmin(lam))])
+        # smoothest mode with a positive eigenvalue: without Dirichlet the constant lies in the
+        # kernel of K0d (sbar would be 0/0 there); DESIGN.md §2 (reading R2-1)
+        pos = np.where(lam > 1e-8 * lam.max())[0]
+        e1.append(V[:, int(pos[np.argmin(lam[pos])])])
         lams.append(lam)
     kron3 = lambda a, b, c: np.kron(c, np.kron(b, a))  # x fastest: (z) (x) (y) (x) (x)
     M0 = kron3(M0d[0], M0d[1], M0d[2])

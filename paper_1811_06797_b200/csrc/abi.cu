@@ -345,8 +345,25 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
         specs[d].push_back({tab, a, b});
         return (int)specs[d].size() - 1;
     };
+    // Q is symmetric when every off-diagonal pair (q_kl, q_lk) carries the same weight (same
+    // R, coefficients and tables); then K = K^T.  Otherwise the KKT matvec needs K^T
+    // separately: block (k,l) of K^T is q_kl with the derivative patterns of block (l,k).
+    auto same_sep = [&](const iga_sep* a, const iga_sep* b) {
+        if (a == b) return true;
+        if (!a || !b || a->R != b->R) return false;
+        for (int r = 0; r < a->R; ++r)
+            if ((a->coef ? a->coef[r] : 1.0) != (b->coef ? b->coef[r] : 1.0)) return false;
+        for (int d = 0; d < 3; ++d)
+            if (a->tab[d] != b->tab[d] && memcmp(a->tab[d], b->tab[d], sizeof(double) * (size_t)a->R * nn[d]) != 0)
+                return false;
+        return true;
+    };
+    bool qsym = true;
+    if (q)
+        for (int k = 0; k < 3; ++k)
+            for (int l = k + 1; l < 3; ++l) qsym = qsym && same_sep(q[k * 3 + l], q[l * 3 + k]);
     // Terms in r-major order: mass r, then stiffness blocks (k,l) for the same r.
-    std::vector<Term> terms;
+    std::vector<Term> terms, termsT;
     int maxR = omega ? omega->R : 0;
     if (q)
         for (int b = 0; b < 9; ++b)
@@ -369,6 +386,11 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
                 for (int d = 0; d < 3; ++d)
                     t.f[d] = factor_id(d, table_id(d, q[b]->tab[d] + (size_t)r * nn[d]), l == d ? 1 : 0, k == d ? 1 : 0);
                 terms.push_back(t);
+                if (!qsym) {  // K^T: (K_kl^(d))^T = pattern (delta(k,d), delta(l,d)) with weight q_kl
+                    for (int d = 0; d < 3; ++d)
+                        t.f[d] = factor_id(d, table_id(d, q[b]->tab[d] + (size_t)r * nn[d]), k == d ? 1 : 0, l == d ? 1 : 0);
+                    termsT.push_back(t);
+                }
             }
     }
 
@@ -388,6 +410,7 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     op->dirichlet = dir;
     op->has_mass = omega != nullptr;
     op->has_stiff = any_q;
+    op->stiff_sym = qsym;
     for (int d = 0; d < 3; ++d) {
         op->n[d] = sp->dir[d].n;
         op->p[d] = sp->dir[d].p;
@@ -418,6 +441,12 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     build_plan(op, terms, true, &op->plan[kPlanBothSplit]);
     build_plan(op, tm, false, &op->plan[kPlanMass]);
     build_plan(op, ts, false, &op->plan[kPlanStiff]);
+    if (!qsym) {
+        std::vector<Term> tmT(tm);
+        tmT.insert(tmT.end(), termsT.begin(), termsT.end());
+        build_plan(op, termsT, false, &op->plan[kPlanStiffT]);
+        build_plan(op, tmT, true, &op->plan[kPlanBothSplitT]);
+    }
     if (fused2_supported(op)) {
         Limits lm;
         lm.x = lm.p = lm.g = lm.e = lm.t = 1;
@@ -436,6 +465,11 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
             build_plan(op, ts, false, &op->plan[kPlanF2Stiff], ls, false);
             if (prepare_fused2(op, &op->plan[kPlanF2Stiff], 1) != IGA_OK) op->plan[kPlanF2Stiff].f2_ok = false;
             prepare_canon(op, &op->plan[kPlanF2Stiff], 1);
+            if (!qsym) {
+                build_plan(op, termsT, false, &op->plan[kPlanF2StiffT], ls, false);
+                if (prepare_fused2(op, &op->plan[kPlanF2StiffT], 1) != IGA_OK) op->plan[kPlanF2StiffT].f2_ok = false;
+                prepare_canon(op, &op->plan[kPlanF2StiffT], 1);
+            }
         }
         g_err.clear();
     }
@@ -483,15 +517,16 @@ static iga_status run_plan(const iga_lr_op* op, PlanKind kind, const OutMap& om,
 // Fused-v2 routing: one launch per part (mass, stiffness); returns IGA_EUNSUPPORTED (no
 // side effects) when a needed part has no fused-v2 plan.
 static iga_status run_f2(const iga_lr_op* op, const double* xm, const double* xs, double* dm, double* ds, double alpha,
-                         double gamma, int batch, cudaStream_t st) {
+                         double gamma, int batch, cudaStream_t st, bool transposed = false) {
     const bool need_m = xm && dm, need_s = xs && ds;
+    const PlanKind sk = transposed ? kPlanF2StiffT : kPlanF2Stiff;
     if (need_m && !op->plan[kPlanF2Mass].f2_ok) return IGA_EUNSUPPORTED;
-    if (need_s && !op->plan[kPlanF2Stiff].f2_ok) return IGA_EUNSUPPORTED;
+    if (need_s && !op->plan[sk].f2_ok) return IGA_EUNSUPPORTED;
     iga_status s = IGA_OK;
     const char* gen = getenv("IGALR_F2_GENERIC");
     const bool canon_ok = !(gen && gen[0] == '1');
     auto part_run = [&](int part, const double* x, double* d, double sc, int acc, cudaStream_t ps) {
-        const Plan& pl = op->plan[part ? kPlanF2Stiff : kPlanF2Mass];
+        const Plan& pl = op->plan[part ? sk : kPlanF2Mass];
         if (canon_ok && pl.canon_ok) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, ps);
         return apply_fused2_part(op, pl, part, x, d, sc, acc, batch, ps);
     };
@@ -534,9 +569,11 @@ static bool want_f2(const iga_lr_op* op, int batch, uint32_t flags) {
     return path == IGA_PATH_AUTO && fused2_preferred(op, batch);
 }
 
-iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out, double alpha,
-                         double gamma, int32_t batch, uint32_t flags, void* stream) {
-    g_err.clear();
+// out = alpha M x_mass + gamma A x_stiff with A = K, or A = K^T when `transposed` (the KKT's
+// calK^T block; the caller checks that the op holds the K^T plans)
+static iga_status apply2_impl(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out,
+                              double alpha, double gamma, int32_t batch, uint32_t flags, void* stream,
+                              bool transposed) {
     if (!op) return set_error(IGA_EINVAL, "op is NULL");
     if (!out) return set_error(IGA_EINVAL, "out is NULL");
     if (batch < 1) return set_error(IGA_EINVAL, "batch < 1");
@@ -549,7 +586,7 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
     if (flags & ~(IGA_PATH_UNFUSED | IGA_PATH_FUSED | 0x40u)) return set_error(IGA_EINVAL, "unknown flags");
     if (want_f2(op, batch, flags)) {
         iga_status s = run_f2(op, x_mass, x_stiff, x_mass ? out : nullptr, x_stiff ? out : nullptr, alpha, gamma, batch,
-                              (cudaStream_t)stream);
+                              (cudaStream_t)stream, transposed);
         if (s != IGA_EUNSUPPORTED) return s;
         g_err.clear();
     }
@@ -561,12 +598,23 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
     om.scale[0] = alpha;
     om.scale[1] = gamma;
     PlanKind kind = (x_mass && x_stiff) ? (x_mass == x_stiff ? kPlanBoth : kPlanBothSplit) : (x_mass ? kPlanMass : kPlanStiff);
+    if (transposed && x_stiff) kind = x_mass ? kPlanBothSplitT : kPlanStiffT;
     if (kind == kPlanMass || kind == kPlanStiff) {
         om.dst[0] = om.dst[1] = out;
         om.src[0] = om.src[1] = x_mass ? x_mass : x_stiff;
     }
     if (kind == kPlanBoth) om.dst[0] = om.dst[1] = out;
+    if (kind == kPlanStiffT) {
+        om.dst[0] = om.dst[1] = out;
+        om.src[0] = om.src[1] = x_stiff;
+    }
     return run_plan(op, kind, om, batch, flags, (cudaStream_t)stream);
+}
+
+iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out, double alpha,
+                         double gamma, int32_t batch, uint32_t flags, void* stream) {
+    g_err.clear();
+    return apply2_impl(op, x_mass, x_stiff, out, alpha, gamma, batch, flags, stream, false);
 }
 
 iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, double* y_stiff, double alpha,
@@ -617,9 +665,16 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     cudaError_t e = cudaMallocAsync(&abc, sizeof(double) * 3 * blk, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
     iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);  // abc = [b, tau a, c]
+    const bool sym = op->stiff_sym;
     const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
+                       (sym || op->plan[kPlanF2StiffT].canon_ok) &&
                        !(getenv("IGALR_F2_GENERIC") && getenv("IGALR_F2_GENERIC")[0] == '1');
-    if (!s && canon) {
+    if (!s && canon && !sym) {
+        // K != K^T: r_y += tau K^T lambda and r_lam += tau K y are two accumulating launches
+        s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
+        if (!s) s = apply_canon_part(op, op->plan[kPlanF2StiffT], 1, in + 2 * blk, out, tau, 1, n_t, st);
+        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
+    } else if (!s && canon) {
         // (r_y, r_u, r_lam) = M [b, tau a, c] in one launch over 3 n_t vectors, then one
         // accumulating stiffness launch over 2 n_t vectors: [lambda, y] -> [r_y, r_lam] (a batch
         // split: vectors n_t.. read y at in and write r_lam at out + 2 blk)
@@ -634,8 +689,8 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
             if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
         }
     } else if (!s) {
-        // r_y = M b + tau S lambda ; r_u = tau M a ; r_lambda = M c + tau S y
-        s = iga_lr_apply2(op, abc, in + 2 * blk, out, 1.0, tau, n_t, flags, stream);
+        // r_y = M b + tau S^T lambda ; r_u = tau M a ; r_lambda = M c + tau S y
+        s = apply2_impl(op, abc, in + 2 * blk, out, 1.0, tau, n_t, flags, stream, !sym);
         if (!s) s = iga_lr_apply2(op, abc + blk, nullptr, out + blk, 1.0, 0.0, n_t, flags, stream);
         if (!s) s = iga_lr_apply2(op, abc + 2 * blk, in, out + 2 * blk, 1.0, tau, n_t, flags, stream);
     }

@@ -86,7 +86,19 @@ struct Plan {
     bool canon_ok = false;
     int canon_mk = 4;               // mass terms per sweep of the canonical mass shape
 };
-enum PlanKind { kPlanBoth = 0, kPlanBothSplit = 1, kPlanMass = 2, kPlanStiff = 3, kPlanF2Mass = 4, kPlanF2Stiff = 5, kNumPlans = 6 };
+// (the *T plans apply K^T = the stiffness with q_kl -> q_lk; built only when Q is not symmetric)
+enum PlanKind {
+    kPlanBoth = 0,
+    kPlanBothSplit = 1,
+    kPlanMass = 2,
+    kPlanStiff = 3,
+    kPlanF2Mass = 4,
+    kPlanF2Stiff = 5,
+    kPlanStiffT = 6,
+    kPlanBothSplitT = 7,
+    kPlanF2StiffT = 8,
+    kNumPlans = 9
+};
 }  // namespace igalr
 
 namespace igalr {
@@ -102,6 +114,9 @@ struct iga_lr_op {
     int n[3], p[3], m[3], nq;
     bool dirichlet;
     bool has_mass, has_stiff;
+    // q_kl and q_lk carry identical weights for every k != l, so K = K^T (the KKT's calK^T block
+    // reuses the K plans); otherwise the *T plans hold K^T (Eq. (KKTSystem))
+    bool stiff_sym = true;
     igalr::DirFactors F[3];
     igalr::DirQuad quad[3];   // (kept for derived operators: the KKT preconditioner)
     igalr::Plan plan[igalr::kNumPlans];

@@ -2,7 +2,7 @@
 //
 // With calM = I (x) M and calK = I (x) tau S + C (x) M (C: 1 on the diagonal, -1 below,
 // PAPER.md:316-318), the three block rows for step k = 1..n_t (y_0 = 0, lambda_{n_t+1} = 0) are
-//   r_y[k]   = tau M y_k + (M + tau S) lambda_k - M lambda_{k+1} = M b_k + tau S lambda_k
+//   r_y[k]   = tau M y_k + (M + tau S)^T lambda_k - M lambda_{k+1} = M b_k + tau S^T lambda_k
 //   r_u[k]   = tau beta M u_k - tau M lambda_k                   = tau M a_k
 //   r_lam[k] = (M + tau S) y_k - M y_{k-1} - tau M u_k          = M c_k + tau S y_k
 // with a_k = beta u_k - lambda_k,  b_k = tau y_k + lambda_k - lambda_{k+1},

@@ -445,7 +445,15 @@ extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, doub
     }
     // scalings: Rayleigh quotients of the op's M and S on the smoothest mode v1 = W e_(i0,j0,k0)
     int i0[3];
-    for (int d = 0; d < 3; ++d) i0[d] = (int)(std::min_element(lam[d].begin(), lam[d].end()) - lam[d].begin());
+    // (smallest POSITIVE eigenvalue: without Dirichlet the constant mode lies in the kernel of
+    // K0d, where the stiffness quotient would be 0/0)
+    for (int d = 0; d < 3; ++d) {
+        const double lmax = *std::max_element(lam[d].begin(), lam[d].end());
+        i0[d] = -1;
+        for (int i = 0; i < (int)lam[d].size(); ++i)
+            if (lam[d][i] > 1e-8 * lmax && (i0[d] < 0 || lam[d][i] < lam[d][i0[d]])) i0[d] = i;
+        if (i0[d] < 0) i0[d] = 0;
+    }
     const int mx = P->m[0], my = P->m[1], mz = P->m[2];
     const size_t N = (size_t)mx * my * mz;
     std::vector<double> v1(N), ym(N), ys(N);

@@ -170,3 +170,74 @@ def test_preconditioned_minres_first_iterate():
     t = (b @ Pinv(Az)) / (Az @ Pinv(Az))
     assert it == 1
     assert np.linalg.norm(x1 - t * z) <= 1e-12 * np.linalg.norm(t * z)
+
+
+# -------------------------------------------------- kkt_prec_dense: the inexact branch pinned
+def _prob(n, p, mass_row, A, amp_v=(0.0, 0.0, 0.0), dirichlet=False):
+    """Problem on a box with distinct extents per direction (a swapped Kronecker order changes
+    the operators) and explicit weights: omega = one term row, Q = v(x) A with v = 1 + amp ..."""
+    knots = [synth.uniform_open_knots(n[d], p) for d in range(3)]
+    v = [0.0, 1.0, 0.0, 0.0, 1.0, 0.0, 0.0, 1.0, 0.0]
+    for d in range(3):
+        v[3 * d] = amp_v[d]
+        v[3 * d + 1] = d + 1.0
+        v[3 * d + 2] = 0.4 * d
+    qt = []
+    for k in range(3):
+        for l in range(3):
+            c = float(A[k][l])
+            qt.append(np.array([[c] + v]) if c != 0.0 else np.zeros((0, 10)))
+    return oracle.Problem(knots=knots, p=[p] * 3, nq=p + 1, mass_terms=np.array([mass_row], dtype=float),
+                          q_terms=qt, dirichlet=dirichlet)
+
+
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_prec_unit_weights_equal_exact(dirichlet):
+    """omega = 1, Q = I (c1's weights) on a 5x6x7 box: M0 = M and S0 = S exactly, so mbar =
+    sbar = 1 and the Kronecker preconditioner IS the exact matching one (a wrong Kronecker
+    order, a wrong pattern or a wrong Dirichlet slice in M0 / S0 breaks the equality)."""
+    one = [1.0, 0, 1, 0, 0, 1, 0, 0, 1, 0]
+    P = _prob((5, 6, 7), 2, one, np.eye(3), dirichlet=dirichlet)
+    M, S = oracle.assemble_csr(P)
+    nt, tau, beta = 2, 0.5, 1e-2
+    Pi, mbar, sbar, _ = oracle.kkt_prec_dense(P, M, S, nt, tau, beta)
+    Pe, _, _, _ = oracle.kkt_prec_dense(P, M, S, nt, tau, beta, exact=True)
+    assert abs(mbar - 1.0) < 1e-13 and abs(sbar - 1.0) < 1e-13
+    assert np.abs(Pi - Pe).max() <= 1e-12 * np.abs(Pe).max()
+
+
+def test_prec_constant_weights_scale():
+    """omega = c, Q = s I: M = c M0 and S = s S0, so mbar = c and sbar = s for any eigenvector
+    choice, and the preconditioner again equals the exact one."""
+    c, s = 2.5, 0.75
+    P = _prob((5, 6, 4), 3, [c, 0, 1, 0, 0, 1, 0, 0, 1, 0], s * np.eye(3))
+    M, S = oracle.assemble_csr(P)
+    Pi, mbar, sbar, _ = oracle.kkt_prec_dense(P, M, S, 2, 0.5, 1e-3)
+    Pe, _, _, _ = oracle.kkt_prec_dense(P, M, S, 2, 0.5, 1e-3, exact=True)
+    assert abs(mbar - c) < 1e-13 * c and abs(sbar - s) < 1e-13 * s
+    assert np.abs(Pi - Pe).max() <= 1e-12 * np.abs(Pe).max()
+
+
+def test_prec_mbar_is_product_of_univariate_rayleigh_quotients():
+    """Separable omega = a(x) b(y) c(z): M = Mz (x) My (x) Mx and v1 = e1z (x) e1y (x) e1x, so
+    mbar = prod_d (e1d' Md e1d) / (e1d' M0d e1d), with e1d the eigenvector of the smallest
+    POSITIVE eigenvalue of K0d v = lam M0d v (computed here with scipy.linalg.eigh on gram_1d).  A wrong
+    eigenvector (e.g. the largest) or a direction mix-up changes mbar by O(1)."""
+    import scipy.linalg as sla_
+    row = [1.0, 0.5, 2.0, 0.3, 0.5, 1.0, 1.1, 0.5, 3.0, 2.0]
+    n, p = (6, 7, 8), 2
+    P = _prob(n, p, row, np.eye(3))
+    M, S = oracle.assemble_csr(P)
+    _, mbar, _, lams = oracle.kkt_prec_dense(P, M, S, 1, 0.5, 1e-2)
+    prod = 1.0
+    for d in range(3):
+        kn = synth.uniform_open_knots(n[d], p)
+        amp, kk, ph = row[1 + 3 * d:4 + 3 * d]
+        Md = oracle.gram_1d(kn, p, p + 1, amp, kk, ph, 0, 0)
+        M0 = oracle.gram_1d(kn, p, p + 1, 0.0, 1.0, 0.0, 0, 0)
+        K0 = oracle.gram_1d(kn, p, p + 1, 0.0, 1.0, 0.0, 1, 1)
+        lam, V = sla_.eigh(K0, M0)  # ascending; lam[0] = 0 (constants) without Dirichlet
+        e = V[:, int(np.argmax(lam > 1e-8 * lam.max()))]  # smoothest mode with lam > 0
+        prod *= (e @ Md @ e) / (e @ M0 @ e)
+        assert np.allclose(np.sort(lams[d]), lam, rtol=1e-12, atol=1e-12)
+    assert abs(mbar - prod) <= 1e-12 * prod

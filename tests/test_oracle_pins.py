@@ -585,3 +585,75 @@ def test_tt_projection_identity_and_symmetry(site):
     B = rng.standard_normal((N, N))
     Ps = oracle.tt_project(B + B.T, gz, gy, gx, site)
     assert np.allclose(Ps, Ps.T, atol=1e-12)
+
+
+# ------------------------------------------------------- KKT with a non-symmetric stiffness
+def _kkt_small_nonsym(nt=3, n=6, seed=11):
+    """Every q_kl is approximated on its own, so q_kl != q_lk is a valid
+    input and K need not be symmetric: scale the (x,y) and (y,z) blocks of A_r only."""
+    cfg = synth.Config(96, "kkt_nonsym", n=n, p=2, R=2, batch=1, dirichlet=True, n_t=nt, tau=1.0 / nt, beta=1e-2)
+    w = synth.draw_weights(cfg, np.random.default_rng(seed))
+    w.A[:, 0, 1] *= 1.7
+    w.A[:, 1, 2] *= -0.5
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    return cfg, P, M, S
+
+
+def test_nonsym_stiffness_is_nonsymmetric_and_transpose_problem_is_its_transpose():
+    """Eq. (stiffnessMatrix) PAPER.md:140-143 with Q^T gives K^T (definition, entry by entry)."""
+    cfg, P, M, S = _kkt_small_nonsym()
+    Sd = S.toarray()
+    assert np.abs(Sd - Sd.T).max() > 1e-3 * np.abs(Sd).max()
+    _, ST = oracle.assemble_csr(oracle.transpose_problem(P))
+    assert np.abs(ST.toarray() - Sd.T).max() < 1e-15 * np.abs(Sd).max() * 10
+    # transposing twice is the identity on the problem
+    _, S2 = oracle.assemble_csr(oracle.transpose_problem(oracle.transpose_problem(P)))
+    assert np.abs(S2.toarray() - Sd).max() == 0.0
+
+
+def test_p9_kkt_symmetric_with_nonsymmetric_stiffness():
+    """Eq. (KKTSystem) PAPER.md:313-319 has calK^T in the first block row, so the KKT matrix
+    is symmetric for ANY K; applying K (instead of K^T) to lambda in the y-row breaks it."""
+    cfg, P, M, S = _kkt_small_nonsym()
+    N = P.ndof
+    dim = 3 * cfg.n_t * N
+    K = np.zeros((dim, dim))
+    for c in range(dim):
+        e = np.zeros(dim)
+        e[c] = 1
+        K[:, c] = oracle.kkt_apply_csr(M, S, e.reshape(3, cfg.n_t, N), cfg.tau, cfg.beta).ravel()
+    assert np.abs(K - K.T).max() < 1e-14 * np.abs(K).max()
+    # ... and equals the block matrix assembled from calK = I (x) tau K + C (x) M (kkt_dense)
+    A = oracle.kkt_dense(M, S, cfg.n_t, cfg.tau, cfg.beta)
+    assert np.abs(K - A).max() < 1e-14 * np.abs(A).max()
+
+
+def test_kkt_apply_equals_dense_nonsym():
+    cfg, P, M, S = _kkt_small_nonsym(nt=4, n=7)
+    N = P.ndof
+    X = np.random.default_rng(12).standard_normal((3, cfg.n_t, N))
+    A = oracle.kkt_dense(M, S, cfg.n_t, cfg.tau, cfg.beta)
+    out = oracle.kkt_apply_csr(M, S, X, cfg.tau, cfg.beta)
+    ref = A @ X.ravel()
+    assert np.linalg.norm(out.ravel() - ref) < 1e-14 * np.linalg.norm(ref)
+    # the y-row carries K^T lambda: with y = u = 0 it is (M + tau K)^T lambda_k - M lambda_{k+1}
+    X0 = np.zeros_like(X)
+    X0[2] = X[2]
+    o0 = oracle.kkt_apply_csr(M, S, X0, cfg.tau, cfg.beta)
+    At = (M + cfg.tau * S).toarray().T
+    for k in range(cfg.n_t):
+        nxt = M @ X[2, k + 1] if k + 1 < cfg.n_t else 0.0
+        assert np.allclose(o0[0, k], At @ X[2, k] - nxt, atol=1e-14)
+
+
+def test_kkt_rows_matches_full_nonsym():
+    cfg, P, M, S = _kkt_small_nonsym(nt=3, n=7)
+    N = P.ndof
+    X = np.random.default_rng(13).standard_normal((3, cfg.n_t, N))
+    full = oracle.kkt_apply_csr(M, S, X, cfg.tau, cfg.beta)
+    rows = np.array([0, 5, N // 2, N - 1])
+    steps = [0, 1, 2]
+    samp = oracle.kkt_rows(P, X, cfg.tau, cfg.beta, steps, rows)
+    for j, k in enumerate(steps):
+        assert np.abs(samp[:, j] - full[:, k][:, rows]).max() < 1e-13 * np.abs(full).max()
