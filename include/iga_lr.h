@@ -224,10 +224,17 @@ typedef struct {
     int32_t has_mass, has_stiff;
     int32_t fused_ok;            /* 1 if the first-generation fused kernel supports this plan */
     int32_t fused2_ok;           /* 1 if the TMEM-ring fused kernel (v2) supports every part */
-    double plan_flops_per_vec;   /* algorithmic flops of one mass+stiffness apply of one vector */
+    /* Algorithmic flops (2 * nnz of every banded mode product) of the plan that
+       the IGA_PATH_AUTO route executes for one vector: the canonical / fused-v2 per-part plans
+       when they exist (reading A: 3R mass + 17R stiffness mode products), else the greedy plans. */
+    double plan_flops_per_vec;   /* mass + stiffness apply of one vector */
     double min_bytes_per_vec;    /* 8 * (1 input + outputs) * N */
     double plan_flops_mass;      /* ... of a mass-only apply of one vector */
     double plan_flops_stiff;     /* ... of a stiffness-only apply of one vector */
+    int32_t canon_mass;          /* 1 if the auto route runs the canonical mass kernel */
+    int32_t canon_stiff;         /* 1 if the auto route runs the canonical (reading-A) stiffness kernel */
+    int32_t stiff_symmetric;     /* 1 if q_kl and q_lk are identical for all k != l (K = K^T) */
+    int32_t f2_rounds_stiff;     /* rounds of the fused-v2 stiffness plan (0 if none) */
 } iga_lr_info_t;
 
 iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info);

@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = (os.environ.get("IGALR_LIB") or os.path.join(_HERE, "libigalr.so"))  # override: experiments only
+LIB_PATH = os.path.join(_HERE, "libigalr.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -40,6 +40,12 @@ ABI_SYMBOLS = ["iga_quad_nodes", "iga_lr_assemble_factors", "iga_lr_destroy", "i
                "iga_weight_lowrank_sep", "iga_weight_lowrank_free", "iga_lr_terms", "iga_tt_kron_apply",
                "iga_tt_interfaces", "iga_tt_local_apply"]
 MINRES_X0 = 0x100
+
+
+class _Knobs(ctypes.Structure):
+    """iga_test_knobs (include/iga_lr_testing.h): test-only kernel-selection overrides."""
+    _fields_ = [("force_generic", ctypes.c_int32), ("qx", ctypes.c_int32), ("minlen", ctypes.c_int32),
+                ("no_yres", ctypes.c_int32), ("no_tma", ctypes.c_int32)]
 
 
 class IgaError(RuntimeError):
@@ -67,7 +73,9 @@ class _Info(ctypes.Structure):
                 ("n_yprod", ctypes.c_int32), ("n_zprod", ctypes.c_int32), ("has_mass", ctypes.c_int32),
                 ("has_stiff", ctypes.c_int32), ("fused_ok", ctypes.c_int32), ("fused2_ok", ctypes.c_int32), ("plan_flops_per_vec", ctypes.c_double),
                 ("min_bytes_per_vec", ctypes.c_double), ("plan_flops_mass", ctypes.c_double),
-                ("plan_flops_stiff", ctypes.c_double)]
+                ("plan_flops_stiff", ctypes.c_double), ("canon_mass", ctypes.c_int32),
+                ("canon_stiff", ctypes.c_int32), ("stiff_symmetric", ctypes.c_int32),
+                ("f2_rounds_stiff", ctypes.c_int32)]
 
 
 class MinresInfo(ctypes.Structure):
@@ -117,6 +125,7 @@ _lib.iga_tt_interfaces.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_
                                    _P, _P, _P]
 _lib.iga_tt_local_apply.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
                                     _P, _P]
+_lib.iga_lr_test_knobs.argtypes = [_P, ctypes.POINTER(_Knobs)]
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -171,13 +180,30 @@ def _stream_handle(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
-def _tensor_ptr(t, name: str) -> int:
+def _tensor_ptr(t, name: str, numel: Optional[int] = None, device: Optional[int] = None) -> int:
+    """data_ptr of a contiguous float64 CUDA tensor holding at least `numel` elements (the extent
+    the library will touch) on CUDA device `device`; ValueError otherwise (an undersized buffer
+    would be written out of bounds by the kernels)."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError("%s must be a torch.Tensor" % name)
     if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
         raise ValueError("%s must be a contiguous float64 CUDA tensor" % name)
+    if numel is not None and t.numel() < numel:
+        raise ValueError("%s has %d elements, the call touches %d" % (name, t.numel(), numel))
+    if device is not None and t.device.index != device:
+        raise ValueError("%s is on cuda:%s, the op on cuda:%d" % (name, t.device.index, device))
     return t.data_ptr()
+
+
+def _host_buf(a: Optional[np.ndarray], name: str, numel: int):
+    if a is None:
+        return None
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError("%s must be a C-contiguous float64 numpy array" % name)
+    if a.size < numel:
+        raise ValueError("%s has %d elements, the call touches %d" % (name, a.size, numel))
+    return a.ctypes.data
 
 
 def greville(knots: np.ndarray, p: int) -> np.ndarray:
@@ -264,6 +290,8 @@ class LowRankOperator:
         self._h = h
         self.info = self._info()
         self.dims = tuple(int(v) for v in self.info.dims)  # (mx, my, mz)
+        import torch
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -285,7 +313,17 @@ class LowRankOperator:
                 "n_rounds": i.n_rounds, "n_xprod": i.n_xprod, "n_yprod": i.n_yprod, "n_zprod": i.n_zprod,
                 "has_mass": bool(i.has_mass), "has_stiff": bool(i.has_stiff), "fused_ok": bool(i.fused_ok), "fused2_ok": bool(i.fused2_ok),
                 "plan_flops_per_vec": i.plan_flops_per_vec, "min_bytes_per_vec": i.min_bytes_per_vec,
-                "plan_flops_mass": i.plan_flops_mass, "plan_flops_stiff": i.plan_flops_stiff}
+                "plan_flops_mass": i.plan_flops_mass, "plan_flops_stiff": i.plan_flops_stiff,
+                "canon_mass": bool(i.canon_mass), "canon_stiff": bool(i.canon_stiff),
+                "stiff_symmetric": bool(i.stiff_symmetric), "f2_rounds_stiff": int(i.f2_rounds_stiff)}
+
+    def _test_knobs(self, force_generic: bool = False, qx: int = 0, minlen: int = 0, no_yres: bool = False,
+                    no_tma: bool = False):
+        """TEST-ONLY: override this op's kernel selection (iga_lr_test_knobs); all defaults
+        restore the product's own choices."""
+        k = _Knobs(int(bool(force_generic)), int(qx), int(minlen), int(bool(no_yres)), int(bool(no_tma)))
+        _check(_lib.iga_lr_test_knobs(self._h, ctypes.byref(k)))
+        self.info = self._info()
 
     def export_factor(self, d: int, fid: int) -> Tuple[np.ndarray, int, int]:
         m = self.dims[d]
@@ -312,48 +350,70 @@ class LowRankOperator:
         per-term cores wz [T, mz, R1] (coefficient folded in), wy [T, R1, my, R2], wx [T, R2, mx]
         (iga_tt_kron_apply)."""
         R1, R2 = int(gy.shape[0]), int(gy.shape[2])
-        _check(_lib.iga_tt_kron_apply(self._h, int(part), R1, R2, _tensor_ptr(gz, "gz"), _tensor_ptr(gy, "gy"),
-                                      _tensor_ptr(gx, "gx"), _tensor_ptr(wz, "wz"), _tensor_ptr(wy, "wy"),
-                                      _tensor_ptr(wx, "wx"), _stream_handle(stream)))
+        mx, my, mz = self.dims
+        T = len(self.terms(part)[1])
+        _check(_lib.iga_tt_kron_apply(self._h, int(part), R1, R2, self._t(gz, "gz", mz * R1),
+                                      self._t(gy, "gy", R1 * my * R2), self._t(gx, "gx", R2 * mx),
+                                      self._t(wz, "wz", T * mz * R1), self._t(wy, "wy", T * R1 * my * R2),
+                                      self._t(wx, "wx", T * R2 * mx), _stream_handle(stream)))
 
     def tt_interfaces(self, part: int, site: int, gz, gy, gx, L, R, stream=None):
         """Frame interfaces of `site` (0 x, 1 y, 2 z) for every term: L [T, Rl, Rl], R [T, Rr, Rr]
         (iga_tt_interfaces)."""
         R1, R2 = int(gy.shape[0]), int(gy.shape[2])
-        _check(_lib.iga_tt_interfaces(self._h, int(part), int(site), R1, R2, _tensor_ptr(gz, "gz"),
-                                      _tensor_ptr(gy, "gy"), _tensor_ptr(gx, "gx"), _tensor_ptr(L, "L"),
-                                      _tensor_ptr(R, "R"), _stream_handle(stream)))
+        mx, my, mz = self.dims
+        T = len(self.terms(part)[1])
+        Rl = (1, R1, R2)[2 - int(site)] if int(site) in (0, 1, 2) else 1
+        Rr = (R1, R2, 1)[2 - int(site)] if int(site) in (0, 1, 2) else 1
+        _check(_lib.iga_tt_interfaces(self._h, int(part), int(site), R1, R2, self._t(gz, "gz", mz * R1),
+                                      self._t(gy, "gy", R1 * my * R2), self._t(gx, "gx", R2 * mx),
+                                      self._t(L, "L", T * Rl * Rl), self._t(R, "R", T * Rr * Rr),
+                                      _stream_handle(stream)))
 
     def tt_local_apply(self, part: int, site: int, L, R, x, y, stream=None):
         """y = (sum_t c_t L_t (x) A_t^(site) (x) R_t) x for local cores x, y [Rl, m_site, Rr]
         (iga_tt_local_apply)."""
-        _check(_lib.iga_tt_local_apply(self._h, int(part), int(site), int(x.shape[0]), int(x.shape[2]),
-                                       _tensor_ptr(L, "L"), _tensor_ptr(R, "R"), _tensor_ptr(x, "x"),
-                                       _tensor_ptr(y, "y"), _stream_handle(stream)))
+        Rl, Rr = int(x.shape[0]), int(x.shape[2])
+        T = len(self.terms(part)[1])
+        m = self.dims[int(site)] if int(site) in (0, 1, 2) else 0
+        _check(_lib.iga_tt_local_apply(self._h, int(part), int(site), Rl, Rr, self._t(L, "L", T * Rl * Rl),
+                                       self._t(R, "R", T * Rr * Rr), self._t(x, "x", Rl * m * Rr),
+                                       self._t(y, "y", Rl * m * Rr), _stream_handle(stream)))
 
     # ------------------------------------------------------------------ device applies
+    def _batch(self, ref, batch: Optional[int]) -> int:
+        if batch is not None:
+            return int(batch)
+        if ref.numel() % self.ndof:
+            raise ValueError("tensor of %d elements is not a batch of %d-DoF vectors" % (ref.numel(), self.ndof))
+        return ref.numel() // self.ndof
+
+    def _t(self, t, name, numel):
+        return _tensor_ptr(t, name, numel, self.device) if t is not None else None
+
     def apply(self, x, y_mass=None, y_stiff=None, alpha: float = 1.0, gamma: float = 1.0, path: str = "auto",
               stream=None, batch: Optional[int] = None):
         """y_mass = alpha M x, y_stiff = gamma S x on device tensors [batch, nz, ny, nx]."""
-        b = batch if batch is not None else (x.numel() // self.ndof)
-        _check(_lib.iga_lr_apply(self._h, _tensor_ptr(x, "x"),
-                                 _tensor_ptr(y_mass, "y_mass") if y_mass is not None else None,
-                                 _tensor_ptr(y_stiff, "y_stiff") if y_stiff is not None else None,
-                                 float(alpha), float(gamma), int(b), PATHS[path], _stream_handle(stream)))
+        b = self._batch(x, batch)
+        n = b * self.ndof
+        _check(_lib.iga_lr_apply(self._h, self._t(x, "x", n), self._t(y_mass, "y_mass", n),
+                                 self._t(y_stiff, "y_stiff", n), float(alpha), float(gamma), int(b), PATHS[path],
+                                 _stream_handle(stream)))
 
     def apply2(self, x_mass, x_stiff, out, alpha: float = 1.0, gamma: float = 1.0, path: str = "auto",
                stream=None, batch: Optional[int] = None):
         ref = x_mass if x_mass is not None else x_stiff
-        b = batch if batch is not None else (ref.numel() // self.ndof)
-        _check(_lib.iga_lr_apply2(self._h, _tensor_ptr(x_mass, "x_mass") if x_mass is not None else None,
-                                  _tensor_ptr(x_stiff, "x_stiff") if x_stiff is not None else None,
-                                  _tensor_ptr(out, "out"), float(alpha), float(gamma), int(b), PATHS[path],
+        b = self._batch(ref, batch)
+        n = b * self.ndof
+        _check(_lib.iga_lr_apply2(self._h, self._t(x_mass, "x_mass", n), self._t(x_stiff, "x_stiff", n),
+                                  self._t(out, "out", n), float(alpha), float(gamma), int(b), PATHS[path],
                                   _stream_handle(stream)))
 
     def kkt_apply(self, X, out, n_t: int, tau: float, beta: float, path: str = "auto", stream=None):
         """out = KKT(tau, beta, n_t) X for device tensors [3, n_t, nz, ny, nx] (Eq. (KKTSystem))."""
-        _check(_lib.iga_kkt_apply(self._h, int(n_t), float(tau), float(beta), _tensor_ptr(X, "X"),
-                                  _tensor_ptr(out, "out"), PATHS[path], _stream_handle(stream)))
+        n = 3 * int(n_t) * self.ndof
+        _check(_lib.iga_kkt_apply(self._h, int(n_t), float(tau), float(beta), self._t(X, "X", n),
+                                  self._t(out, "out", n), PATHS[path], _stream_handle(stream)))
 
     def kkt_minres(self, rhs, x, n_t: int, tau: float, beta: float, rtol: float = 1e-8, maxit: int = 1000,
                    x0: bool = False, prec: "Optional[KKTPreconditioner]" = None, path: str = "auto",
@@ -363,8 +423,9 @@ class LowRankOperator:
         (n_t, tau, beta) or None.  Returns the iga_minres_info record."""
         info = MinresInfo()
         flags = PATHS[path] | (MINRES_X0 if x0 else 0)
+        n = 3 * int(n_t) * self.ndof
         _check(_lib.iga_kkt_minres(self._h, prec._h if prec is not None else None, int(n_t), float(tau), float(beta),
-                                   _tensor_ptr(rhs, "rhs"), _tensor_ptr(x, "x"), float(rtol), int(maxit), flags,
+                                   self._t(rhs, "rhs", n), self._t(x, "x", n), float(rtol), int(maxit), flags,
                                    _stream_handle(stream), ctypes.byref(info)))
         return info
 
@@ -375,18 +436,19 @@ class LowRankOperator:
     # ------------------------------------------------------------------ host (end-to-end) applies
     def apply_host(self, x: np.ndarray, y_mass: Optional[np.ndarray], y_stiff: Optional[np.ndarray],
                    alpha: float = 1.0, gamma: float = 1.0, path: str = "auto", stream=None):
-        for a in (x, y_mass, y_stiff):
-            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous):
-                raise ValueError("host buffers must be C-contiguous float64")
-        b = x.size // self.ndof
-        _check(_lib.iga_lr_apply_host(self._h, x.ctypes.data, y_mass.ctypes.data if y_mass is not None else None,
-                                      y_stiff.ctypes.data if y_stiff is not None else None, float(alpha),
-                                      float(gamma), int(b), PATHS[path], _stream_handle(stream)))
+        if not isinstance(x, np.ndarray) or x.size % self.ndof or x.size == 0:
+            raise ValueError("x must hold a whole batch of %d-DoF vectors" % self.ndof)
+        n = x.size
+        b = n // self.ndof
+        _check(_lib.iga_lr_apply_host(self._h, _host_buf(x, "x", n), _host_buf(y_mass, "y_mass", n),
+                                      _host_buf(y_stiff, "y_stiff", n), float(alpha), float(gamma), int(b),
+                                      PATHS[path], _stream_handle(stream)))
 
     def kkt_apply_host(self, X: np.ndarray, out: np.ndarray, n_t: int, tau: float, beta: float,
                        path: str = "auto", stream=None):
-        _check(_lib.iga_kkt_apply_host(self._h, int(n_t), float(tau), float(beta), X.ctypes.data, out.ctypes.data,
-                                       PATHS[path], _stream_handle(stream)))
+        n = 3 * int(n_t) * self.ndof
+        _check(_lib.iga_kkt_apply_host(self._h, int(n_t), float(tau), float(beta), _host_buf(X, "X", n),
+                                       _host_buf(out, "out", n), PATHS[path], _stream_handle(stream)))
 
 
 class KKTPreconditioner:
@@ -404,7 +466,10 @@ class KKTPreconditioner:
 
     def apply(self, r, out, stream=None):
         """out = P^{-1} r for device tensors [3, n_t, nz, ny, nx]."""
-        _check(_lib.iga_kkt_prec_apply(self._h, _tensor_ptr(r, "r"), _tensor_ptr(out, "out"), _stream_handle(stream)))
+        n = 3 * self.n_t * self.dims[0] * self.dims[1] * self.dims[2]
+        dev = self._op.device
+        _check(_lib.iga_kkt_prec_apply(self._h, _tensor_ptr(r, "r", n, dev), _tensor_ptr(out, "out", n, dev),
+                                       _stream_handle(stream)))
 
     def info(self):
         mb, sb = ctypes.c_double(), ctypes.c_double()

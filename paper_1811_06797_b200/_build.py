@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import os
+import re
 import subprocess
 import sys
 
@@ -20,6 +21,50 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_fused2.cu", "canon_p3.cu",
            "canon_p4.cu", "kkt.cu", "minres.cu", "prec.cu", "weights.cu", "tt.cu"]
+
+
+# Spill guard: the canonical kernels on the bulk-copy + resident-y path (the ones
+# every BASELINE config runs: k_canon<..., YRES=true, TMA=true, ...>) sit near the 255-register
+# cliff, where ptxas flips between 0 and 300+ bytes of spills on unrelated edits.  A build whose
+# ptxas reports spills in one of them fails instead of shipping a silently slower kernel.
+# (Other variants - odd extents, per-round y staging - may spill a few bytes; they are reported.)
+SPILL_RE = re.compile(r"Registers are spilled to local memory in function '([^']+)', (\d+) bytes spill stores, "
+                      r"(\d+) bytes spill loads")
+GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]EEEv")
+# Ratchet: guarded variants that spilled in the round-1 build, with their byte counts (stores,
+# loads).  Any other guarded spill, or growth of these, fails the build.
+_MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dEEEvNS0_5Args2ENS0_6KSplitE"
+KNOWN_SPILLS = {
+    _MK % ("11ShapeStiffA", 3, 16, 2, 1): (12, 20),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0): (12, 28),
+    _MK % ("10ShapeMassKILi4EE", 3, 12, 2, 0): (76, 96),
+    _MK % ("11ShapeStiffA", 4, 13, 4, 0): (56, 72),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 1, 0): (32, 32),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 2, 0): (108, 108),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 4, 0): (100, 100),
+    _MK % ("10ShapeMassKILi4EE", 4, 13, 4, 0): (92, 92),
+    _MK % ("10ShapeMassKILi3EE", 4, 12, 2, 0): (64, 84),
+    _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0): (68, 84),
+}
+
+
+def check_spills(log: str):
+    bad = []
+    for m in SPILL_RE.finditer(log):
+        name, st, ld = m.group(1), int(m.group(2)), int(m.group(3))
+        ks, kl = KNOWN_SPILLS.get(name, (0, 0))
+        if GUARDED.search(name) and (st > ks or ld > kl):
+            bad.append("%s (%d B stores, %d B loads)" % (name, st, ld))
+    if bad:
+        raise RuntimeError("ptxas spilled registers in guarded production kernels:\n  " + "\n  ".join(bad))
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise subprocess.CalledProcessError(r.returncode, cmd[0])
+    return r.stdout + r.stderr
 
 
 def _newer(src_paths, target):
@@ -47,9 +92,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
     # translation units compile in parallel (the canonical-kernel units dominate)
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
-        for rc in ex.map(subprocess.call, jobs):
-            if rc != 0:
-                raise subprocess.CalledProcessError(rc, "nvcc")
+        logs = list(ex.map(_run, jobs))
+    try:
+        check_spills("".join(logs))
+    except RuntimeError:
+        for j in jobs:  # force a rebuild next time (the objects exist but must not ship)
+            try:
+                os.remove(j[-1])
+            except OSError:
+                pass
+        raise
     if force or _newer(objs, LIB):
         tmp = LIB + ".tmp.%d" % os.getpid()
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart=static"]

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "iga_lr_testing.h"
 
 namespace igalr {
 
@@ -160,7 +161,7 @@ struct Limits {
     int x = kMaxX, p = kMaxPair, g = kMaxG, e = kMaxE, t = 1 << 20;  // t: total (pair,group) entries
 };
 
-static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, bool split_slots, Plan* pl,
+static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, bool split_slots, Plan* pl, cudaStream_t st,
                        Limits lim = Limits(), bool fused_v1 = true) {
     // merge identical terms (same part, factors, and slot semantics)
     std::vector<Term> terms;
@@ -248,7 +249,26 @@ static void build_plan(const iga_lr_op* op, const std::vector<Term>& terms_in, b
                        pl->n_y * nnz1(op->m[1], op->p[1]) * (N / op->m[1]) +
                        pl->n_z * nnz1(op->m[2], op->p[2]) * (N / op->m[2]));
     pl->fused_ok = fused_v1 && fused_supported(op, *pl);
-    if (pl->fused_ok && prepare_fused(op, pl) != IGA_OK) pl->fused_ok = false;
+    if (pl->fused_ok && prepare_fused(op, pl, st) != IGA_OK) pl->fused_ok = false;
+}
+
+// Stream-ordered scratch must not return memory to the OS between applies (a release
+// threshold of 0 makes every apply re-map ~100 MB: ms of host time), so each op owns a pool
+// with an infinite threshold instead of changing the device's default pool for the process.
+cudaError_t make_pool(int device, cudaMemPool_t* pool) {
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof props);
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaError_t e = cudaMemPoolCreate(pool, &props);
+    if (e) {
+        *pool = nullptr;
+        return e;
+    }
+    uint64_t thr = ~0ULL;
+    return cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
 static iga_status check_sep(const iga_sep* s, const int* nn, const char* what) {
@@ -397,14 +417,9 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
     iga_lr_op* op = new (std::nothrow) iga_lr_op();
     if (!op) return set_error(IGA_ENOMEM, "host allocation failed");
     cudaGetDevice(&op->device);
-    {
-        // Stream-ordered scratch (cudaMallocAsync) must not return memory to the OS between
-        // applies: a release threshold of 0 makes every apply re-map ~100 MB (ms of host time).
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, op->device) == cudaSuccess) {
-            uint64_t thr = ~0ULL;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
+    if (cudaError_t e = make_pool(op->device, &op->pool)) {
+        delete op;
+        return cuda_error(e, "cudaMemPoolCreate");
     }
     op->nq = sp->nq ? sp->nq : 0;
     op->dirichlet = dir;
@@ -437,15 +452,15 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
             }
         if (!merged) op->kterms.push_back({t.part, {t.f[0], t.f[1], t.f[2]}, t.c});
     }
-    build_plan(op, terms, false, &op->plan[kPlanBoth]);
-    build_plan(op, terms, true, &op->plan[kPlanBothSplit]);
-    build_plan(op, tm, false, &op->plan[kPlanMass]);
-    build_plan(op, ts, false, &op->plan[kPlanStiff]);
+    build_plan(op, terms, false, &op->plan[kPlanBoth], st);
+    build_plan(op, terms, true, &op->plan[kPlanBothSplit], st);
+    build_plan(op, tm, false, &op->plan[kPlanMass], st);
+    build_plan(op, ts, false, &op->plan[kPlanStiff], st);
     if (!qsym) {
         std::vector<Term> tmT(tm);
         tmT.insert(tmT.end(), termsT.begin(), termsT.end());
-        build_plan(op, termsT, false, &op->plan[kPlanStiffT]);
-        build_plan(op, tmT, true, &op->plan[kPlanBothSplitT]);
+        build_plan(op, termsT, false, &op->plan[kPlanStiffT], st);
+        build_plan(op, tmT, true, &op->plan[kPlanBothSplitT], st);
     }
     if (fused2_supported(op)) {
         Limits lm;
@@ -457,24 +472,30 @@ iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, co
         ls.e = 9;
         ls.t = 9;
         if (op->has_mass) {
-            build_plan(op, tm, false, &op->plan[kPlanF2Mass], lm, false);
-            if (prepare_fused2(op, &op->plan[kPlanF2Mass], 0) != IGA_OK) op->plan[kPlanF2Mass].f2_ok = false;
-            prepare_canon(op, &op->plan[kPlanF2Mass], 0);
+            build_plan(op, tm, false, &op->plan[kPlanF2Mass], st, lm, false);
+            if (prepare_fused2(op, &op->plan[kPlanF2Mass], 0, st) != IGA_OK) op->plan[kPlanF2Mass].f2_ok = false;
+            prepare_canon(op, &op->plan[kPlanF2Mass], 0, st);
         }
         if (op->has_stiff) {
-            build_plan(op, ts, false, &op->plan[kPlanF2Stiff], ls, false);
-            if (prepare_fused2(op, &op->plan[kPlanF2Stiff], 1) != IGA_OK) op->plan[kPlanF2Stiff].f2_ok = false;
-            prepare_canon(op, &op->plan[kPlanF2Stiff], 1);
+            build_plan(op, ts, false, &op->plan[kPlanF2Stiff], st, ls, false);
+            if (prepare_fused2(op, &op->plan[kPlanF2Stiff], 1, st) != IGA_OK) op->plan[kPlanF2Stiff].f2_ok = false;
+            prepare_canon(op, &op->plan[kPlanF2Stiff], 1, st);
             if (!qsym) {
-                build_plan(op, termsT, false, &op->plan[kPlanF2StiffT], ls, false);
-                if (prepare_fused2(op, &op->plan[kPlanF2StiffT], 1) != IGA_OK) op->plan[kPlanF2StiffT].f2_ok = false;
-                prepare_canon(op, &op->plan[kPlanF2StiffT], 1);
+                build_plan(op, termsT, false, &op->plan[kPlanF2StiffT], st, ls, false);
+                if (prepare_fused2(op, &op->plan[kPlanF2StiffT], 1, st) != IGA_OK) op->plan[kPlanF2StiffT].f2_ok = false;
+                prepare_canon(op, &op->plan[kPlanF2StiffT], 1, st);
             }
         }
         g_err.clear();
     }
     const double N = (double)op->m[0] * op->m[1] * op->m[2];
     op->min_bytes = 8.0 * N * (1 + (op->has_mass ? 1 : 0) + (op->has_stiff ? 1 : 0));
+    // the plan uploads and z-record kernels are stream-ordered on `stream`: the op is usable
+    // once they land (the call blocks on this stream only, never on the device)
+    if (cudaError_t e = cudaStreamSynchronize(st)) {
+        iga_lr_destroy(op);
+        return cuda_error(e, "assembly");
+    }
     *out = op;
     return IGA_OK;
 }
@@ -495,7 +516,9 @@ void iga_lr_destroy(iga_lr_op* op) {
     for (cudaEvent_t x : op->host_ev) cudaEventDestroy(x);
     for (auto& c : op->fix_cache) {
         if (c.d_tab) cudaFree(c.d_tab);
+        if (c.ready) cudaEventDestroy(c.ready);
     }
+    if (op->pool) cudaMemPoolDestroy(op->pool);
     delete op;
 }
 
@@ -520,14 +543,16 @@ static iga_status run_f2(const iga_lr_op* op, const double* xm, const double* xs
                          double gamma, int batch, cudaStream_t st, bool transposed = false) {
     const bool need_m = xm && dm, need_s = xs && ds;
     const PlanKind sk = transposed ? kPlanF2StiffT : kPlanF2Stiff;
-    if (need_m && !op->plan[kPlanF2Mass].f2_ok) return IGA_EUNSUPPORTED;
-    if (need_s && !op->plan[sk].f2_ok) return IGA_EUNSUPPORTED;
+    // a part runs on the canonical kernel when its plan has the canonical shape, else on the
+    // generic k_fused2 (whose resident round tables bound R); neither => EUNSUPPORTED
+    auto v2 = [&](const Plan& pl) { return pl.canon_ok || pl.f2_ok; };
+    if (need_m && !v2(op->plan[kPlanF2Mass])) return IGA_EUNSUPPORTED;
+    if (need_s && !v2(op->plan[sk])) return IGA_EUNSUPPORTED;
     iga_status s = IGA_OK;
-    const char* gen = getenv("IGALR_F2_GENERIC");
-    const bool canon_ok = !(gen && gen[0] == '1');
+    const bool generic = op->knobs.force_generic != 0;  // (test knob)
     auto part_run = [&](int part, const double* x, double* d, double sc, int acc, cudaStream_t ps) {
         const Plan& pl = op->plan[part ? sk : kPlanF2Mass];
-        if (canon_ok && pl.canon_ok) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, ps);
+        if (pl.canon_ok && !(generic && pl.f2_ok)) return apply_canon_part(op, pl, part, x, d, sc, acc, batch, ps);
         return apply_fused2_part(op, pl, part, x, d, sc, acc, batch, ps);
     };
     if (need_m && need_s && dm != ds && canon_small_grid(op, batch)) {
@@ -662,13 +687,12 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     const int64_t N = (int64_t)op->m[0] * op->m[1] * op->m[2];
     const size_t blk = (size_t)n_t * N;
     double* abc = nullptr;  // a, b, c combos [3][n_t][N]
-    cudaError_t e = cudaMallocAsync(&abc, sizeof(double) * 3 * blk, st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&abc, sizeof(double) * 3 * blk, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
     iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);  // abc = [b, tau a, c]
     const bool sym = op->stiff_sym;
     const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
-                       (sym || op->plan[kPlanF2StiffT].canon_ok) &&
-                       !(getenv("IGALR_F2_GENERIC") && getenv("IGALR_F2_GENERIC")[0] == '1');
+                       (sym || op->plan[kPlanF2StiffT].canon_ok) && !op->knobs.force_generic;
     if (!s && canon && !sym) {
         // K != K^T: r_y += tau K^T lambda and r_lam += tau K y are two accumulating launches
         s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
@@ -698,11 +722,11 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     return s;
 }
 
-static iga_status host_roundtrip(size_t in_elems, size_t out_elems, int nout, const double* in_h, double** out_h,
-                                 cudaStream_t st, double** d_in, double** d_out) {
-    cudaError_t e = cudaMallocAsync(d_in, sizeof(double) * in_elems, st);
+static iga_status host_roundtrip(const iga_lr_op* op, size_t in_elems, size_t out_elems, int nout, const double* in_h,
+                                 double** out_h, cudaStream_t st, double** d_in, double** d_out) {
+    cudaError_t e = pool_alloc(op->pool, (void**)d_in, sizeof(double) * in_elems, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(host in)");
-    e = cudaMallocAsync(d_out, sizeof(double) * out_elems * nout, st);
+    e = pool_alloc(op->pool, (void**)d_out, sizeof(double) * out_elems * nout, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(host out)");
     e = cudaMemcpyAsync(*d_in, in_h, sizeof(double) * in_elems, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_error(e, "H2D");
@@ -726,8 +750,8 @@ iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* 
     double *d_in = nullptr, *d_out = nullptr;
     const bool same = y_mass_host && y_mass_host == y_stiff_host;
     int nout = same ? 1 : (y_mass_host ? 1 : 0) + (y_stiff_host ? 1 : 0);
-    cudaError_t e = cudaMallocAsync(&d_in, sizeof(double) * tot, st);
-    if (!e) e = cudaMallocAsync(&d_out, sizeof(double) * tot * nout, st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&d_in, sizeof(double) * tot, st);
+    if (!e) e = pool_alloc(op->pool, (void**)&d_out, sizeof(double) * tot * nout, st);
     if (e) {
         if (d_in) cudaFreeAsync(d_in, st);
         return cuda_error(e, "cudaMallocAsync(host apply)");
@@ -805,7 +829,7 @@ iga_status iga_kkt_apply_host(const iga_lr_op* op, int32_t n_t, double tau, doub
     cudaStream_t st = (cudaStream_t)stream;
     const size_t tot = (size_t)op->m[0] * op->m[1] * op->m[2] * n_t * 3;
     double *d_in = nullptr, *d_out = nullptr;
-    iga_status s = host_roundtrip(tot, tot, 1, in_host, nullptr, st, &d_in, &d_out);
+    iga_status s = host_roundtrip(op, tot, tot, 1, in_host, nullptr, st, &d_in, &d_out);
     if (!s) s = iga_kkt_apply(op, n_t, tau, beta, d_in, d_out, flags, stream);
     cudaError_t e = cudaSuccess;
     if (!s) e = cudaMemcpyAsync(out_host, d_out, sizeof(double) * tot, cudaMemcpyDeviceToHost, st);
@@ -836,11 +860,33 @@ iga_status iga_lr_info(const iga_lr_op* op, iga_lr_info_t* info) {
     info->has_mass = op->has_mass;
     info->has_stiff = op->has_stiff;
     info->fused_ok = pl.fused_ok;
-    info->fused2_ok = (!op->has_mass || op->plan[kPlanF2Mass].f2_ok) && (!op->has_stiff || op->plan[kPlanF2Stiff].f2_ok);
-    info->plan_flops_per_vec = pl.flops;
+    auto v2 = [&](const Plan& p) { return p.canon_ok || p.f2_ok; };
+    info->fused2_ok = (!op->has_mass || v2(op->plan[kPlanF2Mass])) && (!op->has_stiff || v2(op->plan[kPlanF2Stiff]));
     info->min_bytes_per_vec = op->min_bytes;
-    info->plan_flops_mass = op->has_mass ? op->plan[kPlanMass].flops : 0.0;
-    info->plan_flops_stiff = op->has_stiff ? op->plan[kPlanStiff].flops : 0.0;
+    // flops of the plans the auto route executes (fused-v2 per-part plans when they exist)
+    const Plan& f2m = op->plan[kPlanF2Mass];
+    const Plan& f2s = op->plan[kPlanF2Stiff];
+    const bool f2 = info->fused2_ok && fused2_preferred(op, 1);
+    info->plan_flops_mass = op->has_mass ? (f2 ? f2m.flops : op->plan[kPlanMass].flops) : 0.0;
+    info->plan_flops_stiff = op->has_stiff ? (f2 ? f2s.flops : op->plan[kPlanStiff].flops) : 0.0;
+    info->plan_flops_per_vec = f2 ? info->plan_flops_mass + info->plan_flops_stiff : pl.flops;
+    info->canon_mass = op->has_mass && f2 && f2m.canon_ok;
+    info->canon_stiff = op->has_stiff && f2 && f2s.canon_ok;
+    info->stiff_symmetric = op->stiff_sym;
+    info->f2_rounds_stiff = op->has_stiff && v2(f2s) ? (int32_t)f2s.rounds.size() : 0;
+    return IGA_OK;
+}
+
+iga_status iga_lr_test_knobs(iga_lr_op* op, const iga_test_knobs* k) {
+    g_err.clear();
+    if (!op || !k) return set_error(IGA_EINVAL, "NULL argument");
+    if (k->qx != 0 && k->qx != 1 && k->qx != 2 && k->qx != 4) return set_error(IGA_EINVAL, "qx must be 0, 1, 2 or 4");
+    if (k->minlen < 0) return set_error(IGA_EINVAL, "minlen < 0");
+    op->knobs.force_generic = k->force_generic != 0;
+    op->knobs.qx = k->qx;
+    op->knobs.minlen = k->minlen;
+    op->knobs.no_yres = k->no_yres != 0;
+    op->knobs.no_tma = k->no_tma != 0;
     return IGA_OK;
 }
 

@@ -281,7 +281,7 @@ bool fused_supported(const iga_lr_op* op, const Plan& pl) {
     return true;
 }
 
-iga_status prepare_fused(const iga_lr_op* op, Plan* pl) {
+iga_status prepare_fused(const iga_lr_op* op, Plan* pl, cudaStream_t st) {
     (void)op;
     std::vector<FRound> fr(pl->rounds.size());
     int nslot = 1;
@@ -319,7 +319,8 @@ iga_status prepare_fused(const iga_lr_op* op, Plan* pl) {
     pl->fused_part = parts_seen[1] && !parts_seen[0] ? 1 : 0;
     cudaError_t e = cudaMalloc(&pl->d_fused, sizeof(FRound) * fr.size());
     if (e) return cuda_error(e, "cudaMalloc(fused rounds)");
-    e = cudaMemcpy(pl->d_fused, fr.data(), sizeof(FRound) * fr.size(), cudaMemcpyHostToDevice);
+    // (pageable source: staged before the call returns; assembly synchronises `st` at its end)
+    e = cudaMemcpyAsync(pl->d_fused, fr.data(), sizeof(FRound) * fr.size(), cudaMemcpyHostToDevice, st);
     if (e) return cuda_error(e, "fused rounds H2D");
     return IGA_OK;
 }

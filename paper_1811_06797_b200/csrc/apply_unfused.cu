@@ -98,9 +98,9 @@ iga_status apply_unfused(const iga_lr_op* op, const Plan& pl, const OutMap& om, 
     const long long tot = d.N * batch;
     double* T = nullptr;
     double* U = nullptr;
-    cudaError_t e = cudaMallocAsync(&T, sizeof(double) * (size_t)tot * kMaxX, st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&T, sizeof(double) * (size_t)tot * kMaxX, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(T)");
-    e = cudaMallocAsync(&U, sizeof(double) * (size_t)tot * kMaxPair, st);
+    e = pool_alloc(op->pool, (void**)&U, sizeof(double) * (size_t)tot * kMaxPair, st);
     if (e != cudaSuccess) {
         cudaFreeAsync(T, st);
         return cuda_error(e, "cudaMallocAsync(U)");

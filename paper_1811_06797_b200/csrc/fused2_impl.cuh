@@ -1389,7 +1389,7 @@ cudaError_t launch2(const iga_lr_op* op, const Plan& pl, const double* src, doub
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * L * TX;
-    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    e = pool_alloc(op->pool, (void**)&a.scratch, sizeof(double) * scratch_elems, st);
     if (e) return e;
     kern<<<a.nctas, NW * 32, sm, st>>>(a);
     e = cudaGetLastError();
@@ -1542,7 +1542,7 @@ struct CanonCfg {
 struct TileChoice {
     int qx, lw;
 };
-static TileChoice pick_tile(int mx, int my, int P) {
+static TileChoice pick_tile(int mx, int my, int P, int qx_override = 0) {
     const int LW0 = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
     // p = 3 also weighs 48-row tiles (LW 12, QX 2); p = 4 weighs LW 13 (26-row tiles, 234 of a
     // warp's 256 TMEM columns with the 9-double ring): 256 rows tile as 10 x 26 instead of 11 x 24
@@ -1560,15 +1560,13 @@ static TileChoice pick_tile(int mx, int my, int P) {
             best = cand[i];
         }
     }
-    const char* s = getenv("IGALR_QX");
-    if (s && (s[0] == '1' || s[0] == '2' || s[0] == '4')) best = {s[0] - '0', LW0};
+    if (qx_override == 1 || qx_override == 2 || qx_override == 4) best = {qx_override, LW0};  // (test knob)
     return best;
 }
 
 // minimum planes per persistent CTA range (see launch_canon_t)
-static long long canon_minlen(long long units, int P, int sms) {
-    const char* ml = getenv("IGALR_MINLEN");  // (experiment knob)
-    if (ml) return std::max(1LL, atoll(ml));
+static long long canon_minlen(const iga_lr_op* op, long long units, int P, int sms) {
+    if (op->knobs.minlen > 0) return op->knobs.minlen;  // (test knob)
     return units >= (long long)sms * (2 * P + 2) ? 2 * P + 2 : 1;
 }
 
@@ -1585,7 +1583,8 @@ static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, c
         if (std::equal(key, key + 9, c.key)) {
             *tab = static_cast<const f2::FixEnt*>(c.d_tab);
             *n = c.n;
-            return cudaSuccess;
+            // the upload may have been queued on another stream: order this launch after it
+            return c.ready ? cudaStreamWaitEvent(st, c.ready, 0) : cudaSuccess;
         }
     std::map<std::pair<long long, int>, f2::FixEnt> ents;
     const long long TYX = (long long)a.tyt * a.txt;
@@ -1620,11 +1619,19 @@ static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, c
     std::copy(key, key + 9, c.key);
     c.n = (int)v.size();
     c.d_tab = nullptr;
+    c.ready = nullptr;
     if (!v.empty()) {
         cudaError_t e = cudaMalloc(&c.d_tab, v.size() * sizeof(f2::FixEnt));
-        // (pageable source: the copy is staged before the call returns, then runs in stream order)
+        // (pageable source: the copy is staged before the call returns, then runs in stream order;
+        // the event orders users on other streams after it)
         if (!e) e = cudaMemcpyAsync(c.d_tab, v.data(), v.size() * sizeof(f2::FixEnt), cudaMemcpyHostToDevice, st);
-        if (e) return e;
+        if (!e) e = cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming);
+        if (!e) e = cudaEventRecord(c.ready, st);
+        if (e) {
+            if (c.d_tab) cudaFree(c.d_tab);
+            if (c.ready) cudaEventDestroy(c.ready);
+            return e;
+        }
     }
     op->fix_cache.push_back(c);
     *tab = static_cast<const f2::FixEnt*>(c.d_tab);
@@ -1666,7 +1673,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     // CTA ranges of >= 2P+2 planes keep the fixup volume (2P partial planes per range boundary)
     // small; a mesh with fewer units than that takes one CTA per unit instead (every plane then has
     // up to 2P+1 contributors, which the table-driven fixup sums): parallelism wins there (c2).
-    const long long minlen = canon_minlen(a.units, P, sms);
+    const long long minlen = canon_minlen(op, a.units, P, sms);
     if (a.units / nct < minlen) nct = a.units / minlen;
     if (nct < 1) nct = 1;
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
@@ -1680,7 +1687,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
-    e = cudaMallocAsync(&a.scratch, sizeof(double) * scratch_elems, st);
+    e = pool_alloc(op->pool, (void**)&a.scratch, sizeof(double) * scratch_elems, st);
     if (e) return e;
     int nfix = 0;
     const f2::FixEnt* tab = nullptr;
@@ -1725,13 +1732,11 @@ size_t canon_smem(int p, int nrounds) {
 template <class S, int P, int QX, int LW = CanonCfg<P>::LW>
 cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
-    const char* s = getenv("IGALR_YRES");
-    const bool force_off = s && s[0] == '0';
-    const char* t = getenv("IGALR_TMA");
+    const bool force_off = op->knobs.no_yres != 0;
     // TMA needs 16-byte row strides (even nx), 16-byte aligned input and the driver entry point
     // bulk copies need 16-byte aligned coefficient rows: (factor * nx + x0) * BW even <=> nx even
     // the GSYNC path (TMA && YRES) also bulk-copies plane rows: 16-byte aligned input
-    const bool tma = !(t && t[0] == '0') && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
+    const bool tma = !op->knobs.no_tma && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
     const bool yres = !force_off && yres_fits<S, P, QX, LW>(pl.canon_nrounds);
     if (sp.bsplit) {
         // batch split (KKT stiffness): p = 3 stiffness on the GSYNC path only; otherwise the
@@ -1766,7 +1771,7 @@ cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const
 template <class S, int P>
 cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
-    const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, op->knobs.qx);
     if constexpr (P == 3) {
         if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
@@ -1815,14 +1820,14 @@ __global__ void k_build_ztab(const double* __restrict__ bz, const int* __restric
 }
 
 template <class S>
-iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
+iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl, cudaStream_t st) {
     std::vector<f2::RoundC<S>> v;
     if (!build_canon<S>(op, *pl, &v)) return IGA_EUNSUPPORTED;
     const int n = (int)v.size();
     if (canon_smem<S>(op->p[0], n) > 227 * 1024) return IGA_EUNSUPPORTED;
     cudaError_t e = cudaMalloc(&pl->d_canon, sizeof(v[0]) * n);
     if (e) return cuda_error(e, "cudaMalloc(canon rounds)");
-    e = cudaMemcpy(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice);
+    e = cudaMemcpyAsync(pl->d_canon, v.data(), sizeof(v[0]) * n, cudaMemcpyHostToDevice, st);
     if (e) return cuda_error(e, "canon rounds H2D");
     // per-plane z records (GSYNC path)
     const int P = op->p[2], BW = 2 * P + 1, mz = op->m[2];
@@ -1838,17 +1843,20 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
     double* d_gs = nullptr;
     const size_t nz = (size_t)mz * n * ngb;
     e = cudaMalloc(&pl->d_ztab, sizeof(double) * nz);
-    if (!e) e = cudaMalloc(&d_gf, sizeof(int) * gf.size());
-    if (!e) e = cudaMalloc(&d_gs, sizeof(double) * gs.size());
-    if (!e) e = cudaMemcpy(d_gf, gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice);
-    if (!e) e = cudaMemcpy(d_gs, gs.data(), sizeof(double) * gs.size(), cudaMemcpyHostToDevice);
+    if (!e) e = pool_alloc(op->pool, (void**)&d_gf, sizeof(int) * gf.size(), st);
+    if (!e) e = pool_alloc(op->pool, (void**)&d_gs, sizeof(double) * gs.size(), st);
+    if (!e) e = cudaMemcpyAsync(d_gf, gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(d_gs, gs.data(), sizeof(double) * gs.size(), cudaMemcpyHostToDevice, st);
     if (!e) {
-        k_build_ztab<<<(unsigned)((nz + 255) / 256), 256>>>(op->F[2].band, d_gf, d_gs, n, S::NG, ngb, mz, P, pl->d_ztab);
+        k_build_ztab<<<(unsigned)((nz + 255) / 256), 256, 0, st>>>(op->F[2].band, d_gf, d_gs, n, S::NG, ngb, mz, P,
+                                                                  pl->d_ztab);
         e = cudaGetLastError();
     }
-    if (!e) e = cudaDeviceSynchronize();
-    cudaFree(d_gf);
-    cudaFree(d_gs);
+    // stream-ordered temporaries (cudaFree would synchronise the device); the host tables die
+    // here, so wait for this stream
+    if (d_gf) cudaFreeAsync(d_gf, st);
+    if (d_gs) cudaFreeAsync(d_gs, st);
+    if (!e) e = cudaStreamSynchronize(st);
     if (e) return cuda_error(e, "canon z records");
     pl->canon_nrounds = n;
     pl->canon_ok = true;
@@ -1857,15 +1865,16 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl) {
 
 }  // namespace
 
-iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part) {
+iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st) {
     if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
     if (part == 0) {
         // mass terms per sweep: 4, or 3 when that avoids zero-padding terms (e.g. R = 6)
         const int R = (int)pl->rounds.size();
         pl->canon_mk = (R % 4 != 0 && R % 3 == 0) ? 3 : 4;
-        return pl->canon_mk == 3 ? prepare_canon_t<f2::ShapeMassK<3>>(op, pl) : prepare_canon_t<f2::ShapeMassK<4>>(op, pl);
+        return pl->canon_mk == 3 ? prepare_canon_t<f2::ShapeMassK<3>>(op, pl, st)
+                                 : prepare_canon_t<f2::ShapeMassK<4>>(op, pl, st);
     }
-    return prepare_canon_t<f2::ShapeStiffA>(op, pl);
+    return prepare_canon_t<f2::ShapeStiffA>(op, pl, st);
 }
 
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
@@ -1889,7 +1898,7 @@ bool canon_small_grid(const iga_lr_op* op, int batch) {
     // both parts' persistent grids fit the GPU side by side: launch them concurrently
     if (!fused2_supported(op)) return false;
     const int P = op->p[0];
-    const TileChoice tc = pick_tile(op->m[0], op->m[1], P);
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, op->knobs.qx);
     const long long tx = 32 * tc.qx, ty = (long long)tc.lw * 2 * (4 / tc.qx);
     const long long units = (op->m[0] + tx - 1) / tx * ((op->m[1] + ty - 1) / ty) * batch * op->m[2];
     int dev = 0, sms = 148;
@@ -1899,15 +1908,13 @@ bool canon_small_grid(const iga_lr_op* op, int batch) {
 }
 
 bool fused2_preferred(const iga_lr_op* op, int batch) {
-    // 128-wide tiles: narrow meshes waste lanes; small meshes cannot fill the persistent grid
-    // persistent CTAs need enough (tile, plane) units to fill the GPU
-    const long long N = (long long)op->m[0] * op->m[1] * op->m[2] * batch;
-    const char* s = getenv("IGALR_F2_MIN");
-    const long long thr = s ? atoll(s) : 0;
-    return N >= thr;
+    // every mesh size: small meshes take one CTA per (tile, plane) unit (canon_small_grid)
+    (void)op;
+    (void)batch;
+    return true;
 }
 
-iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part) {
+iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st) {
     if (!fused2_supported(op)) return IGA_EUNSUPPORTED;
     size_t bytes = 0;
     std::vector<char> blob;
@@ -1935,7 +1942,8 @@ iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part) {
     if (sm > 227 * 1024) return IGA_EUNSUPPORTED;
     cudaError_t e = cudaMalloc(&pl->d_f2, bytes);
     if (e) return cuda_error(e, "cudaMalloc(f2 rounds)");
-    e = cudaMemcpy(pl->d_f2, blob.data(), bytes, cudaMemcpyHostToDevice);
+    e = cudaMemcpyAsync(pl->d_f2, blob.data(), bytes, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaStreamSynchronize(st);  // (blob is a local)
     if (e) return cuda_error(e, "f2 rounds H2D");
     pl->f2_ok = true;
     return IGA_OK;

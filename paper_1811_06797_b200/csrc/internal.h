@@ -117,6 +117,15 @@ struct iga_lr_op {
     // q_kl and q_lk carry identical weights for every k != l, so K = K^T (the KKT's calK^T block
     // reuses the K plans); otherwise the *T plans hold K^T (Eq. (KKTSystem))
     bool stiff_sym = true;
+    // kernel-selection overrides for tests and experiments (iga_lr_test_knobs, include/
+    // iga_lr_testing.h); all zero => the product's own choices
+    struct Knobs {
+        int force_generic = 0;  // 1: fused-v2 parts run k_fused2 even when a canonical plan exists
+        int qx = 0;             // 1/2/4: canonical tile width in 32-column quadrants
+        int minlen = 0;         // > 0: persistent-CTA range length in planes
+        int no_yres = 0;        // 1: per-round y-coefficient staging
+        int no_tma = 0;         // 1: no bulk-copy staging
+    } knobs;
     igalr::DirFactors F[3];
     igalr::DirQuad quad[3];   // (kept for derived operators: the KKT preconditioner)
     igalr::Plan plan[igalr::kNumPlans];
@@ -128,6 +137,7 @@ struct iga_lr_op {
         long long key[9];
         void* d_tab;
         int n;
+        cudaEvent_t ready;  // recorded after the table's upload; every user waits on it
     };
     mutable std::mutex fix_mu;
     mutable std::vector<FixCache> fix_cache;
@@ -138,9 +148,18 @@ struct iga_lr_op {
     mutable std::mutex host_mu;
     mutable cudaStream_t host_sh = nullptr, host_sd = nullptr;
     mutable std::vector<cudaEvent_t> host_ev;
+    // op-owned stream-ordered memory pool for all scratch (release threshold: never), so that
+    // scratch stays mapped between applies without touching the device's default pool
+    cudaMemPool_t pool = nullptr;
 };
 
 namespace igalr {
+
+// ---- stream-ordered scratch from an owned pool (abi.cu make_pool)
+cudaError_t make_pool(int device, cudaMemPool_t* pool);
+inline cudaError_t pool_alloc(cudaMemPool_t pool, void** p, size_t bytes, cudaStream_t st) {
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
 
 // ---- error plumbing (abi.cu)
 iga_status set_error(iga_status s, const std::string& msg);
@@ -160,13 +179,13 @@ iga_status assemble_dir(const DirQuad& q, const std::vector<std::vector<double>>
 iga_status apply_unfused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
 iga_status apply_fused(const iga_lr_op* op, const Plan& pl, const OutMap& om, int batch, cudaStream_t st);
 bool fused_supported(const iga_lr_op* op, const Plan& pl);
-iga_status prepare_fused(const iga_lr_op* op, Plan* pl);
+iga_status prepare_fused(const iga_lr_op* op, Plan* pl, cudaStream_t st);
 void release_fused(Plan* pl);
 bool fused2_supported(const iga_lr_op* op);
 bool fused2_preferred(const iga_lr_op* op, int batch);
 bool canon_small_grid(const iga_lr_op* op, int batch);
-iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part);
-iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part);
+iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st);
+iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st);
 // Batch split of a canonical launch (KKT): vectors b >= bsplit are read at src + b*vol + src_jump
 // and written at dst + b*vol + dst_jump (element offsets).  The default is the plain batch.
 struct CanonSplit {

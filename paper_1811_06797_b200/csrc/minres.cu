@@ -180,7 +180,7 @@ extern "C" iga_status iga_kkt_minres(const iga_lr_op* op, const iga_kkt_prec* pr
     double* ws = nullptr;
     const size_t vec = (size_t)n;
     const int nvec = prec ? 8 : 7;
-    cudaError_t e = cudaMallocAsync(&ws, sizeof(double) * (nvec * vec + kDotBlocks) + sizeof(MinresState), st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&ws, sizeof(double) * (nvec * vec + kDotBlocks) + sizeof(MinresState), st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(minres)");
     double* v_prev = ws;
     double* v = ws + vec;

@@ -33,6 +33,7 @@ struct iga_kkt_prec {
     double* dAt[3];  // V_d'
     double* dlam[3];
     int device;
+    cudaMemPool_t pool = nullptr;  // scratch of iga_kkt_prec_apply (kept mapped)
 };
 
 namespace igalr {
@@ -403,6 +404,10 @@ extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, doub
     cudaStream_t st = (cudaStream_t)stream;
     iga_kkt_prec* P = new iga_kkt_prec();
     memset(P, 0, sizeof *P);
+    if (cudaError_t e0 = make_pool(op->device, &P->pool)) {
+        delete P;
+        return cuda_error(e0, "cudaMemPoolCreate");
+    }
     P->n_t = n_t;
     P->tau = tau;
     P->beta = beta;
@@ -423,7 +428,8 @@ extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, doub
             return s;
         }
         std::vector<double> band((size_t)2 * m * F.bw);
-        cudaError_t e = cudaMemcpy(band.data(), F.band, sizeof(double) * band.size(), cudaMemcpyDeviceToHost);
+        cudaError_t e = cudaMemcpyAsync(band.data(), F.band, sizeof(double) * band.size(), cudaMemcpyDeviceToHost, st);
+        if (!e) e = cudaStreamSynchronize(st);
         cudaFree(F.band);
         if (e) {
             iga_kkt_prec_destroy(P);
@@ -463,18 +469,18 @@ extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, doub
                 v1[((size_t)z * my + y) * mx + x] =
                     V[2][(size_t)z * mz + i0[2]] * V[1][(size_t)y * my + i0[1]] * V[0][(size_t)x * mx + i0[0]];
     double* dv = nullptr;
-    cudaError_t e = cudaMalloc(&dv, sizeof(double) * 3 * N);
-    if (!e) e = cudaMemcpy(dv, v1.data(), sizeof(double) * N, cudaMemcpyHostToDevice);
+    cudaError_t e = pool_alloc(P->pool, (void**)&dv, sizeof(double) * 3 * N, st);
+    if (!e) e = cudaMemcpyAsync(dv, v1.data(), sizeof(double) * N, cudaMemcpyHostToDevice, st);
     iga_status s = IGA_OK;
     if (e) s = cuda_error(e, "prec scaling");
     if (!s) s = iga_lr_apply(op, dv, dv + N, dv + 2 * N, 1.0, 1.0, 1, flags, stream);
     if (!s) {
-        e = cudaStreamSynchronize(st);
-        if (!e) e = cudaMemcpy(ym.data(), dv + N, sizeof(double) * N, cudaMemcpyDeviceToHost);
-        if (!e) e = cudaMemcpy(ys.data(), dv + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost);
+        e = cudaMemcpyAsync(ym.data(), dv + N, sizeof(double) * N, cudaMemcpyDeviceToHost, st);
+        if (!e) e = cudaMemcpyAsync(ys.data(), dv + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, st);
+        if (!e) e = cudaStreamSynchronize(st);
         if (e) s = cuda_error(e, "prec scaling");
     }
-    cudaFree(dv);
+    if (dv) cudaFreeAsync(dv, st);
     if (s) {
         iga_kkt_prec_destroy(P);
         return s;
@@ -498,9 +504,10 @@ extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, doub
         e = cudaMalloc(&P->dA[d], sizeof(double) * m * m);
         if (!e) e = cudaMalloc(&P->dAt[d], sizeof(double) * m * m);
         if (!e) e = cudaMalloc(&P->dlam[d], sizeof(double) * m);
-        if (!e) e = cudaMemcpy(P->dA[d], V[d].data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
-        if (!e) e = cudaMemcpy(P->dAt[d], At.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice);
-        if (!e) e = cudaMemcpy(P->dlam[d], lam[d].data(), sizeof(double) * m, cudaMemcpyHostToDevice);
+        if (!e) e = cudaMemcpyAsync(P->dA[d], V[d].data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st);
+        if (!e) e = cudaMemcpyAsync(P->dAt[d], At.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice, st);
+        if (!e) e = cudaMemcpyAsync(P->dlam[d], lam[d].data(), sizeof(double) * m, cudaMemcpyHostToDevice, st);
+        if (!e) e = cudaStreamSynchronize(st);  // (At is a local)
         if (e) {
             iga_kkt_prec_destroy(P);
             return cuda_error(e, "prec upload");
@@ -517,6 +524,7 @@ extern "C" void iga_kkt_prec_destroy(iga_kkt_prec* P) {
         if (P->dAt[d]) cudaFree(P->dAt[d]);
         if (P->dlam[d]) cudaFree(P->dlam[d]);
     }
+    if (P->pool) cudaMemPoolDestroy(P->pool);
     delete P;
 }
 
@@ -527,7 +535,7 @@ extern "C" iga_status iga_kkt_prec_apply(const iga_kkt_prec* P, const double* in
     cudaStream_t st = (cudaStream_t)stream;
     const size_t tot = (size_t)3 * P->n_t * P->m[0] * P->m[1] * P->m[2];
     double* tmp = nullptr;
-    cudaError_t e = cudaMallocAsync(&tmp, sizeof(double) * tot, st);
+    cudaError_t e = pool_alloc(P->pool, (void**)&tmp, sizeof(double) * tot, st);
     if (e) return cuda_error(e, "cudaMallocAsync(prec)");
     iga_status s = kkt_prec_apply(P, in, out, tmp, st);
     cudaFreeAsync(tmp, st);

@@ -239,9 +239,9 @@ iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, in
     const size_t big = (size_t)T * R1 * my * R2;
     const size_t small = (size_t)T * (size_t)std::max({R1 * R1, R2 * R2, R2 * mx, R1 * mz});
     double *s1 = nullptr, *s2 = nullptr, *s3 = nullptr;
-    cudaError_t e = cudaMallocAsync(&s1, sizeof(double) * big, st);
-    if (!e) e = cudaMallocAsync(&s2, sizeof(double) * big, st);
-    if (!e) e = cudaMallocAsync(&s3, sizeof(double) * small, st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&s1, sizeof(double) * big, st);
+    if (!e) e = pool_alloc(op->pool, (void**)&s2, sizeof(double) * big, st);
+    if (!e) e = pool_alloc(op->pool, (void**)&s3, sizeof(double) * small, st);
     if (!e) {
         if (site == 1) {  // L over z, R over x
             e = left_of_y(op, tz, R1, gz, L, s3, st);
@@ -250,7 +250,7 @@ iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, in
             k_fill<<<grid_for(T), 256, 0, st>>>(L, T, 1.0);
             double* Rx = s3;  // [T][R2][R2]
             double* tx_buf = nullptr;  // the x mode product [T][R2][mx]
-            e = cudaMallocAsync(&tx_buf, sizeof(double) * (size_t)T * R2 * mx, st);
+            e = pool_alloc(op->pool, (void**)&tx_buf, sizeof(double) * (size_t)T * R2 * mx, st);
             if (!e) e = right_of_y(op, tx, R2, gx, Rx, tx_buf, st);
             if (!e) e = mode(op, 1, ty, false, gy, 0, s1, R1, R2, st);  // Hy[t][a'][iy][b']
             if (!e) {
@@ -269,7 +269,7 @@ iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, in
             k_fill<<<grid_for(T), 256, 0, st>>>(R, T, 1.0);
             double* Lz = s3;  // [T][R1][R1]
             double* tz_buf = nullptr;
-            e = cudaMallocAsync(&tz_buf, sizeof(double) * (size_t)T * R1 * mz, st);
+            e = pool_alloc(op->pool, (void**)&tz_buf, sizeof(double) * (size_t)T * R1 * mz, st);
             if (!e) e = left_of_y(op, tz, R1, gz, Lz, tz_buf, st);
             if (!e) e = mode(op, 1, ty, false, gy, 0, s1, R1, R2, st);  // Hy[t][a'][iy][b']
             if (!e) {
@@ -305,8 +305,8 @@ iga_status iga_tt_local_apply(const iga_lr_op* op, int32_t part, int32_t site, i
     const int m = op->m[site], T = tab.T;
     const size_t per = (size_t)Rl * m * Rr;
     double *a = nullptr, *b = nullptr;
-    cudaError_t e = cudaMallocAsync(&a, sizeof(double) * per * T, st);
-    if (!e) e = cudaMallocAsync(&b, sizeof(double) * per * T, st);
+    cudaError_t e = pool_alloc(op->pool, (void**)&a, sizeof(double) * per * T, st);
+    if (!e) e = pool_alloc(op->pool, (void**)&b, sizeof(double) * per * T, st);
     if (!e) {
         // a[t][r'][j][s] = sum_{s'} R_t[s][s'] x[r'][j][s']   (x shared by all terms)
         k_tt_right<<<grid_for((long long)per * T), 256, 0, st>>>(x, 0, R, a, T, Rl, m, Rr);

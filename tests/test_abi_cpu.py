@@ -18,8 +18,8 @@ def igalr():
     return m
 
 
-def _declared_symbols():
-    hdr = open(os.path.join(ROOT, "include", "iga_lr.h")).read()
+def _declared_symbols(header="iga_lr.h"):
+    hdr = open(os.path.join(ROOT, "include", header)).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
     return sorted(set(re.findall(r"\b(iga_[a-z0-9_]+)\s*\(", hdr)))
 
@@ -31,6 +31,22 @@ def test_header_symbols_exported(igalr):
     for n in names:
         assert hasattr(lib, n), "missing export " + n
     assert set(names) == set(igalr.ABI_SYMBOLS)
+
+
+def test_testing_header_symbols_exported(igalr):
+    """include/iga_lr_testing.h (test-only kernel-selection knobs) is exported too, and the
+    product binding no longer takes its library path from the environment."""
+    lib = ctypes.CDLL(igalr.LIB_PATH)
+    names = _declared_symbols("iga_lr_testing.h")
+    assert names == ["iga_lr_test_knobs"]
+    assert hasattr(lib, "iga_lr_test_knobs")
+    assert igalr.LIB_PATH == os.path.join(ROOT, "paper_1811_06797_b200", "libigalr.so")
+    src = open(os.path.join(ROOT, "paper_1811_06797_b200", "__init__.py")).read()
+    assert "environ" not in src
+    # and no kernel-selection environment variable is read anywhere in the library sources
+    csrc = os.path.join(ROOT, "paper_1811_06797_b200", "csrc")
+    for f in os.listdir(csrc):
+        assert "getenv" not in open(os.path.join(csrc, f)).read(), f
 
 
 def test_version_and_last_error(igalr):

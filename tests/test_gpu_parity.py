@@ -177,15 +177,15 @@ def test_full_size_sampled_rows(env, cfgname):
 
 
 @pytest.mark.parametrize("minlen", [1, 2, 3, 5])
-def test_fixup_table_many_contributors(env, minlen, monkeypatch):
-    """Persistent-CTA ranges of `minlen` planes (IGALR_MINLEN, an experiment knob) give output
-    planes with up to 2P+1 contributors in the table-driven fixup; every setting matches the
-    oracle (the summation order, not the result, depends on the split)."""
+def test_fixup_table_many_contributors(env, minlen):
+    """Persistent-CTA ranges of `minlen` planes (the test-only knob of iga_lr_testing.h) give
+    output planes with up to 2P+1 contributors in the table-driven fixup; every setting matches
+    the oracle (the summation order, not the result, depends on the split)."""
     torch, igalr, workloads = env
-    monkeypatch.setenv("IGALR_MINLEN", str(minlen))
     cfg = synth.scaled(synth.CONFIGS["c3"], 21, batch=2)
     knots, w, x = synth.draw_problem(cfg)
     op = workloads.build_operator(cfg, w)
+    op._test_knobs(minlen=minlen)
     yM, yS = gpu_apply(env, op, x, "auto")
     P = oracle.problem_from_config(cfg, w)
     M, S = oracle.assemble_csr(P)

@@ -138,3 +138,168 @@ def test_prec_scalings_unit_weights(env, dirichlet):
     _, mo, so, _ = oracle.kkt_prec_dense(P2, M2, S2, 1, 0.5, 1e-2)
     mg, sg, _ = op2.kkt_preconditioner(1, 0.5, 1e-2).info()
     assert abs(mg - mo) <= 1e-12 * mo and abs(sg - so) <= 1e-12 * so
+
+
+# ----------------------------------------------------------------- non-canonical stiffness weights
+def build_custom(igalr, knots, p, mass_terms, q_terms, dirichlet=False):
+    """LowRankOperator from synth-format term rows: omega = mass_terms, q_kl = q_terms[k*3+l]
+    (None / empty => zero block), each tabulated at the library's quadrature nodes."""
+    nodes = igalr.quad_nodes(knots, [p] * 3)
+    omega = igalr.SepWeight(mass_terms[:, 0], synth.tabulate(mass_terms, nodes))
+    q = []
+    for t in q_terms:
+        q.append(None if t is None or len(t) == 0 else igalr.SepWeight(t[:, 0], synth.tabulate(t, nodes)))
+    return igalr.LowRankOperator(knots, [p] * 3, omega, q, dirichlet=dirichlet)
+
+
+def draw_terms(rng, R, coef_lo=1.0, coef_hi=2.0):
+    t = np.zeros((R, 10))
+    t[:, 0] = rng.uniform(coef_lo, coef_hi, R)
+    for r in range(R):
+        for d in range(3):
+            t[r, 1 + 3 * d:4 + 3 * d] = (0.5, rng.integers(1, 5), rng.uniform(0, 2 * np.pi))
+    return t
+
+
+def recipe(kind, R, seed):
+    """Stiffness weights that are not reading A of G6:
+       diag: q_kk = sum_r a_kr v_r (one shared v_r per r), off-diagonal blocks zero;
+       iso:  Q = v I (q_xx = q_yy = q_zz, same table and coefficients);
+       B:    reading B: independent rank-R tables per upper-triangle block, q_lk = q_kl;
+       Bns:  reading B without the symmetry (all nine blocks independent)."""
+    rng = np.random.default_rng(seed)
+    mass = draw_terms(rng, R)
+    q = [None] * 9
+    if kind in ("diag", "iso"):
+        v = draw_terms(rng, R)
+        for k in range(3):
+            t = v.copy()
+            if kind == "diag":
+                t[:, 0] = rng.uniform(1.0, 2.0, R)
+            q[k * 3 + k] = t
+    elif kind == "B":
+        for k in range(3):
+            for l in range(k, 3):
+                t = draw_terms(rng, R, *((1.0, 2.0) if k == l else (-0.3, 0.3)))
+                q[k * 3 + l] = t
+                q[l * 3 + k] = t
+    else:
+        for b in range(9):
+            q[b] = draw_terms(rng, R, *((1.0, 2.0) if b in (0, 4, 8) else (-0.3, 0.3)))
+    return mass, q
+
+
+_ORC = {}
+
+
+@pytest.mark.parametrize("kind", ["diag", "iso", "B", "Bns"])
+@pytest.mark.parametrize("p,n", [(3, 37), (3, 44), (4, 30), (4, 27)])
+@pytest.mark.parametrize("path", ["fused", "auto"])
+def test_noncanonical_weights_full_vector(env, kind, p, n, path):
+    """Full-vector parity for weights the canonical reading-A kernel does not take (it needs all
+    nine (y,x) pairs of one shared v_r table): these run the generic fused kernel k_fused2 (or
+    the unfused path) — asserted through iga_lr_info — against the oracle's element loop."""
+    torch, igalr, workloads = env
+    R = 2
+    mass, q = recipe(kind, R, 100 * p + n)
+    knots = [synth.uniform_open_knots(n, p)] * 3
+    op = build_custom(igalr, knots, p, mass, q)
+    inf = op.info_dict()
+    assert not inf["canon_stiff"], inf  # the generic kernel is what is under test
+    assert inf["f2_rounds_stiff"] > 0, inf
+    assert inf["stiff_symmetric"] == (kind != "Bns")
+    x = np.random.default_rng(n).standard_normal((2, n, n, n))
+    key = (kind, p, n)
+    if key not in _ORC:
+        P = oracle.Problem(knots=knots, p=[p] * 3, nq=p + 1, mass_terms=mass,
+                           q_terms=[np.zeros((0, 10)) if t is None else t for t in q])
+        _ORC[key] = oracle.apply_matfree(P, x)
+    rm, rs = _ORC[key]
+    xd = torch.from_numpy(x).cuda()
+    ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+    op.apply(xd, ym, ys, path=path)
+    gm, gs = ym.cpu().numpy(), ys.cpu().numpy()
+    for b in range(2):
+        assert rel(gm[b], rm[b]) <= TOL
+        assert rel(gs[b], rs[b]) <= TOL
+        assert np.linalg.norm(gs[b]) > 1e-3 * np.linalg.norm(x[b])  # S x is not trivially 0
+
+
+@pytest.mark.parametrize("R", [12, 24, 48])
+@pytest.mark.parametrize("p,n", [(3, 36), (3, 33), (4, 28)])
+def test_large_rank_full_vector(env, R, p, n):
+    """Reading-A weights of rank R = 12, 24, 48 (the paper's ranks reach 36 for one q entry and
+    R1 R2 = 29 x 14 for TT weights): per-round y-coefficient staging
+    (the resident table no longer fits shared memory), odd extents (no bulk-copy path) and the
+    R > 40 fallback of the fused-v2 plans."""
+    torch, igalr, workloads = env
+    cfg = dataclasses.replace(synth.scaled(synth.CONFIGS["c2"], n), R=R, p=p)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    inf = op.info_dict()
+    assert inf["canon_stiff"] == (R <= 40), inf
+    P = oracle.problem_from_config(cfg, w)
+    x = np.random.default_rng(R + n).standard_normal((1, n, n, n))
+    rm, rs = oracle.apply_matfree(P, x)
+    xd = torch.from_numpy(x).cuda()
+    ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+    op.apply(xd, ym, ys)
+    assert rel(ym.cpu().numpy(), rm) <= TOL
+    assert rel(ys.cpu().numpy(), rs) <= TOL
+
+
+# ----------------------------------------------------------------- full arrays at BASELINE size
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_array_baseline_size(env, name):
+    """Every output of every batch vector at the BASELINE size, in the launch configuration
+    bench.py times, against the oracle's element-loop bilinear forms (Eqs. (massMatrix) /
+    (stiffnessMatrix)): c3 (8 x 128^3) and c5 (256^3, p = 4)."""
+    torch, igalr, workloads = env
+    cfg = synth.CONFIGS[name]
+    knots, w, x = synth.draw_problem(cfg)
+    op = workloads.build_operator(cfg, w)
+    P = oracle.problem_from_config(cfg, w)
+    xd = torch.from_numpy(x).cuda()
+    ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+    op.apply(xd, ym, ys)
+    gm, gs = ym.cpu().numpy(), ys.cpu().numpy()
+    del xd, ym, ys
+    for b in range(cfg.batch):
+        rm, rs = oracle.apply_matfree(P, x[b])
+        assert rel(gm[b], rm) <= TOL, (b, rel(gm[b], rm))
+        assert rel(gs[b], rs) <= TOL, (b, rel(gs[b], rs))
+
+
+# ----------------------------------------------------------------- binding argument checks
+def test_binding_rejects_undersized_buffers(env):
+    """The binding checks every extent the library will touch: undersized device
+    tensors and host arrays raise ValueError before any kernel runs."""
+    torch, igalr, workloads = env
+    cfg = synth.scaled(synth.CONFIGS["c4"], 8, n_t=2)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    N = op.ndof
+    x = torch.zeros((2, N), dtype=torch.float64, device="cuda")
+    small = torch.zeros((N,), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        op.apply(x, small, None)                       # y_mass holds 1 of 2 vectors
+    with pytest.raises(ValueError):
+        op.apply(torch.zeros((N + 1,), dtype=torch.float64, device="cuda"), small, None)  # not a batch
+    with pytest.raises(ValueError):
+        op.apply2(x, x, small)
+    X = torch.zeros((3, 2, N), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        op.kkt_apply(X, X[:2].contiguous(), 2, cfg.tau, cfg.beta)
+    with pytest.raises(ValueError):
+        op.kkt_apply(X, torch.empty_like(X), 3, cfg.tau, cfg.beta)  # n_t larger than the buffers
+    with pytest.raises(ValueError):
+        op.apply_host(np.zeros(2 * N), np.zeros(N), None)
+    with pytest.raises(ValueError):
+        op.apply_host(np.zeros(N + 3), np.zeros(N + 3), None)
+    with pytest.raises(ValueError):
+        op.kkt_apply_host(np.zeros(6 * N), np.zeros(5 * N), 2, cfg.tau, cfg.beta)
+    # correctly sized calls still work
+    op.apply(x, torch.empty_like(x), torch.empty_like(x))
+    op.kkt_apply(X, torch.empty_like(X), 2, cfg.tau, cfg.beta)
+    torch.cuda.synchronize()

@@ -171,3 +171,42 @@ def test_gpu_op_from_annulus_weights(igalr):
     op.apply(one, ym, ys)
     assert abs(float(ym.sum()) - vol) <= 1e-12 * vol
     assert float(ys.abs().max()) <= 1e-12 * float(ym.abs().max()) * n
+    # ... and S x is not trivially zero for a random x
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal((1, n, n, n))).cuda()
+    op.apply(x, ym, ys)
+    assert float(ys.norm()) > 1e-2 * float(x.norm())
+
+
+@pytest.mark.gpu
+def test_gpu_op_from_library_weights_vs_oracle_weights(igalr):
+    """NEXT-2 end to end: the op assembled from the LIBRARY's low-rank annulus weights
+    (iga_weight_lowrank: TT-SVD + collocation solves) applied on the GPU, against
+    the oracle's element-loop forms with the ORACLE's own low-rank weights (oracle.weight_lowrank)
+    given at every 3D quadrature point (Problem.weights3d): rel l2 <= 1e-11 for M x and S x."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    pt, nt = 3, 10
+    tk, om, qs, vol = annulus(pt, nt)
+    n, p = 20, 3
+    kn = synth.uniform_open_knots(n, p)
+    knots = [kn] * 3
+    omega, _, _ = igalr.weight_lowrank(knots, [p] * 3, tk, [pt] * 3, om, eps=1e-12)
+    q = [None] * 9
+    for i, qq in enumerate(qs):
+        q[i * 3 + i], _, _ = igalr.weight_lowrank(knots, [p] * 3, tk, [pt] * 3, qq, eps=1e-12)
+    op = igalr.LowRankOperator(knots, [p] * 3, omega, q)
+    nodes = [oracle.quad_nodes(kn, p, p + 1)] * 3
+    w3 = np.zeros((10, len(nodes[2]), len(nodes[1]), len(nodes[0])))
+    w3[0] = grid_eval(oracle.weight_lowrank(nodes, tk, [pt] * 3, om, 1e-12)[0])
+    for i, qq in enumerate(qs):
+        w3[1 + i * 3 + i] = grid_eval(oracle.weight_lowrank(nodes, tk, [pt] * 3, qq, 1e-12)[0])
+    P = oracle.Problem(knots=knots, p=[p] * 3, nq=p + 1, mass_terms=None, q_terms=None, weights3d=w3)
+    x = np.random.default_rng(11).standard_normal((1, n, n, n))
+    rm, rs = oracle.apply_matfree(P, x)
+    xd = torch.from_numpy(x).cuda()
+    ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+    op.apply(xd, ym, ys)
+    for got, ref in ((ym, rm), (ys, rs)):
+        g = got.cpu().numpy()
+        assert np.linalg.norm(g - ref) <= 1e-11 * np.linalg.norm(ref)
