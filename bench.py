@@ -11,7 +11,8 @@ configs (c2, c4 KKT, c5) are timed the same way and reported under "configs".
 
 Multi-GPU (torchrun, one process per GPU): every rank applies its own batch (weak scaling, the
 batch dimension shards with no collective); time = max over ranks.
---impl reference times the CPU oracle (row-restricted bilinear form) on the host cores.
+--impl reference times the CPU oracle (CSR SpMV of a one-plane row sample of the same workload,
+the assembled full-size matrices' rows) on the host cores.
 """
 from __future__ import annotations
 
@@ -42,25 +43,69 @@ def _measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region by a background thread that
+    polls NVML every `period_s` (2 ms: a 20-step c3 region of ~30 ms still gets ~15 samples).
+    Falls back to `nvidia-smi -lms 10` when NVML is unavailable."""
 
-    def __init__(self, index: int):
+    _REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.rows = []
+        self.period = period_s
+        self.rows = []  # (sm_mhz, sm_max_mhz, power_w, reasons bitmask)
         self.proc = None
+        self.stop = threading.Event()
+        self.t = None
+        self.source = "nvml"
+
+    def _poll_nvml(self, nv, h):
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((float(sm), float(mx), pw, int(rs)))
+            except Exception:
+                pass
+            self.stop.wait(self.period)
+
+    def _read_smi(self):
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.proc.stdout:
+            r = [v.strip() for v in line.split(",")]
+            try:
+                bits = sum(self._REASONS[n] for i, n in enumerate(names) if r[3 + i] == "Active")
+                self.rows.append((float(r[0]), float(r[1]), float(r[2]), bits))
+            except Exception:
+                pass
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 2.0:
+                time.sleep(0.001)
+            self.rows = []
+            return self
+        except Exception:
+            pass
+        self.source = "nvidia-smi"
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
-            # nvidia-smi takes a while to start: wait for its first sample so that the timed
-            # region (which starts when this returns) is covered
             t0 = time.time()
             while not self.rows and time.time() - t0 < 5.0:
                 time.sleep(0.01)
@@ -69,29 +114,25 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([s.strip() for s in line.split(",")])
-
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.t:
             self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "source": self.source}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n, b in self._REASONS.items() if r[3] & b})
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "power_w_max": max(r[2] for r in self.rows), "samples": len(self.rows),
+                "source": self.source}
 
 
 def dist_setup(backend: str = "nccl"):
@@ -266,28 +307,75 @@ def measured_traffic(workload: str):
 
 
 # ----------------------------------------------------------------------------------- CPU arm
-def cpu_oracle_rate(cfgname: str, seconds: float = 12.0):
-    """Oracle (row-restricted bilinear form, OpenMP on all host cores) on a bounded sample of
-    rows of the workload: GDoF/s = output rows (mass+stiffness) per second."""
-    import oracle
-    cfg = synth.CONFIGS[cfgname]
-    knots, w, x = synth.draw_problem(cfg)
-    P = oracle.problem_from_config(cfg, w)
-    rng = np.random.default_rng(0)
-    N = P.ndof
-    done = 0
-    t0 = time.perf_counter()
-    chunk = 256
-    xv = x.reshape(-1, N) if not cfg.kkt else x.reshape(-1, N)
-    while time.perf_counter() - t0 < seconds:
-        rows = rng.integers(0, N, chunk)
-        oracle.apply_rows(P, xv[done // chunk % xv.shape[0]], rows)
-        done += chunk
-    el = time.perf_counter() - t0
+class OracleSample:
+    """The CPU oracle on a bounded sample of a workload, the way SURVEY §8(d) times it: the rows of
+    `planes` z-planes of the full-size matrices are assembled by tensor Gauss quadrature
+    (oracle.assemble_csr_rows; assembly timed separately) and applied by the oracle's naive CSR
+    SpMV to the workload's own input vector.  A c4 (KKT) step is the paper's three rows per time
+    step on those spatial rows: 3 mass + 2 stiffness SpMVs (oracle.kkt_apply's work per step)."""
+
+    def __init__(self, cfgname: str, planes: int = 1):
+        import oracle
+        self.oracle = oracle
+        self.cfg = cfg = synth.CONFIGS[cfgname]
+        knots, w, x = synth.draw_problem(cfg)
+        self.P = P = oracle.problem_from_config(cfg, w)
+        N = P.ndof
+        mx, my, mz = P.dims
+        z0 = mz // 2
+        self.r0, self.r1 = z0 * mx * my, min(mz, z0 + planes) * mx * my
+        oracle.set_threads(0)
+        t0 = time.perf_counter()
+        self.M, self.S = oracle.assemble_csr_rows(P, self.r0, self.r1)
+        self.assembly_s = time.perf_counter() - t0
+        self.x = np.ascontiguousarray(x.reshape(-1, N)[0])
+        self.rows = self.r1 - self.r0
+        # DoFs one step processes: rows x (1 for the apply's M and S outputs; 3 blocks for a KKT step)
+        self.dof = self.rows * (3 if cfg.kkt else 1)
+        self.sample = ("rows [%d, %d) (%d z-planes) of the full-size %s matrices (CSR, %d nnz per matrix), "
+                       "one input vector" % (self.r0, self.r1, planes, cfg.name, self.M.nnz))
+
+    def step(self):
+        sp = self.oracle.spmv
+        if self.cfg.kkt:
+            for _ in range(3):
+                sp(self.M, self.x)
+            for _ in range(2):
+                sp(self.S, self.x)
+        else:
+            sp(self.M, self.x)
+            sp(self.S, self.x)
+
+    def rate(self, threads: int, reps: int = 3) -> float:
+        """GDoF/s at `threads` OpenMP threads (0 = all cores): median of `reps` after 1 warm-up."""
+        self.oracle.set_threads(threads)
+        self.step()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            self.step()
+            ts.append(time.perf_counter() - t0)
+        self.oracle.set_threads(0)
+        return self.dof / statistics.median(ts) / 1e9
+
+
+def cpu_baseline(cfgname: str, matfree: bool = True):
+    """cpu_baseline of the JSON line: oracle CSR SpMV at all cores (value) and at
+    1 thread, assembly time separately; plus (c3) the matrix-free element-loop route on one full
+    vector at all cores."""
     cores = len(os.sched_getaffinity(0))
-    kind_rows = done * (1 if not cfg.kkt else 1)
-    return {"value": kind_rows / el / 1e9, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
-            "sample": "%d random output rows (mass+stiffness) of %s, %.1f s" % (done, cfgname, el)}
+    s = OracleSample(cfgname)
+    v_all = s.rate(0)
+    v_one = s.rate(1)
+    out = {"value": v_all, "unit": "GDoF/s", "cores": cores, "kind": "oracle", "route": "csr_spmv",
+           "sample": s.sample, "value_1thread": v_one, "assembly_s_sample": s.assembly_s,
+           "assembly_rows_per_s": s.rows / s.assembly_s}
+    if matfree and not s.cfg.kkt and s.P.ndof <= 4 * 1024 * 1024:
+        t0 = time.perf_counter()
+        s.oracle.apply_matfree(s.P, s.x.reshape(1, *s.x.shape))
+        out["matfree_value"] = s.P.ndof / (time.perf_counter() - t0) / 1e9
+        out["matfree_sample"] = "one full %s vector, element loop, all cores" % s.cfg.name
+    return out
 
 
 def time_kkt_solve(rtol: float = 1e-8):
@@ -376,7 +464,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "unfused"])
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     a = ap.parse_args()
     warmup = max(3, a.warmup)
 
@@ -385,16 +473,25 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        per = []
-        for _ in range(max(1, min(a.steps, 3))):
-            per.append(cpu_oracle_rate(a.config, seconds=max(2.0, a.cpu_seconds / 3)))
-        val = statistics.median(p["value"] for p in per)
+        # the CPU oracle on the host cores: each step = the CSR SpMVs of a bounded sample (one
+        # z-plane of rows) of the same workload; assembly of the sample runs once, untimed
+        cores = len(os.sched_getaffinity(0))
+        s = OracleSample(a.config)
+        for _ in range(warmup):
+            s.step()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            s.step()
+        el = time.perf_counter() - t0
+        val = s.dof * a.steps / el / 1e9
         cfg = synth.CONFIGS[a.config]
         line = {"metric": "GDoF/s of fp64 low-rank Kronecker operator/KKT apply; % of roofline",
-                "impl": "reference", "value": val, "unit": "GDoF/s", "n_gpus": a.gpus, "steps": len(per),
-                "warmup": 0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": cfg.name, "global_batch": cfg.batch},
-                "cpu_baseline": dict(per[0], value=val),
+                "impl": "reference", "value": val, "unit": "GDoF/s", "n_gpus": a.gpus, "steps": a.steps,
+                "warmup": warmup, "ms_per_step": 1e3 * el / a.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg.name, "global_batch": cfg.batch},
+                "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
+                                 "route": "csr_spmv", "sample": s.sample, "assembly_s_sample": s.assembly_s},
                 "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -466,8 +563,8 @@ def main():
         except Exception as e:  # report, never hide
             extra["c4_solve"] = {"error": repr(e)}
         line["configs"] = extra
-    if rank == 0 and ws == 1:
-        line["cpu_baseline"] = cpu_oracle_rate(a.config, seconds=a.cpu_seconds)
+    if rank == 0 and ws == 1 and not a.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(a.config)
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:

@@ -84,6 +84,11 @@ def _L():
         common = [I, I, D, D, D, ctypes.c_int, ctypes.c_int, D, I, D, ctypes.c_int, D]
         lib.orc_assemble_csr.argtypes = common + [I64, I32, D, D]
         lib.orc_spmv.argtypes = [ctypes.c_int64, I64, I32, D, D, D]
+        lib.orc_assemble_csr_rows.argtypes = common + [ctypes.c_int64, ctypes.c_int64, I64, I32, D, D]
+        lib.orc_csr_rows_nnz.argtypes = [I, I, ctypes.c_int, ctypes.c_int64, ctypes.c_int64]
+        lib.orc_csr_rows_nnz.restype = ctypes.c_int64
+        lib.orc_set_threads.argtypes = [ctypes.c_int]
+        lib.orc_set_threads.restype = None
         lib.orc_apply_matfree.argtypes = common + [D, D, D]
         lib.orc_apply_rows.argtypes = common + [D, ctypes.c_int64, I64, D, D]
         _lib = lib
@@ -230,6 +235,31 @@ def assemble_csr(P: Problem, mass: bool = True, stiff: bool = True):
     M = sp.csr_matrix((vm, col, rowptr), shape=(N, N)) if mass else None
     S = sp.csr_matrix((vs, col, rowptr), shape=(N, N)) if stiff else None
     return M, S
+
+
+def assemble_csr_rows(P: Problem, r0: int, r1: int, mass: bool = True, stiff: bool = True):
+    """Rows [r0, r1) of (M, S) as scipy.sparse.csr_matrix of shape (r1-r0, N): the same
+    assembly as assemble_csr restricted to a row range (bench samples of full-size matrices)."""
+    import scipy.sparse as sp
+    N = P.ndof
+    nnz = _L().orc_csr_rows_nnz(_ip(P._n), _ip(P._p), int(P.dirichlet), int(r0), int(r1))
+    rowptr = np.zeros(r1 - r0 + 1, dtype=np.int64)
+    col = np.zeros(nnz, dtype=np.int32)
+    vm = np.zeros(nnz) if mass else None
+    vs = np.zeros(nnz) if stiff else None
+    rc = _L().orc_assemble_csr_rows(*P._args(), int(r0), int(r1),
+                                    rowptr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                    col.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dp(vm), _dp(vs))
+    if rc:
+        raise ValueError("oracle row assembly failed")
+    M = sp.csr_matrix((vm, col, rowptr), shape=(r1 - r0, N)) if mass else None
+    S = sp.csr_matrix((vs, col, rowptr), shape=(r1 - r0, N)) if stiff else None
+    return M, S
+
+
+def set_threads(t: int = 0):
+    """OpenMP threads of the oracle (0 = all cores)."""
+    _L().orc_set_threads(int(t))
 
 
 def spmv(A, x: np.ndarray) -> np.ndarray:

@@ -363,32 +363,34 @@ int64_t orc_csr_nnz(const int* n, const int* p, int dirichlet) {
  *   M_ij = sum_{elements E} sum_{points} W omega beta_i beta_j
  *   S_ij = sum_E sum_pts W sum_kl q_kl d_l beta_i d_k beta_j
  */
-int orc_assemble_csr(const int* n, const int* p, const double* kx, const double* ky, const double* kz,
-                     int nq, int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
-                     int dirichlet, const double* w3, int64_t* rowptr, int32_t* colidx, double* valM, double* valS) {
-    const double* knots[3] = {kx, ky, kz};
-    orc_prob P;
-    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3)) {
-        orc_prob_free(&P);
-        return 1;
-    }
-    const int mx = P.m[0], my = P.m[1], mz = P.m[2];
-    const int64_t nrows = (int64_t)mx * my * mz;
+int orc_assemble_csr_rows(const int* n, const int* p, const double* kx, const double* ky, const double* kz,
+                          int nq, int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
+                          int dirichlet, const double* w3, int64_t r0, int64_t r1, int64_t* rowptr, int32_t* colidx,
+                          double* valM, double* valS);
+
+/* rows [r0, r1) of the kept DoFs: rowptr[0..r1-r0] local to the range, global column indices */
+static int orc_assemble_rows(const orc_prob* Pp, int64_t r0, int64_t r1, int nq, int64_t* rowptr, int32_t* colidx,
+                             double* valM, double* valS) {
+    const orc_prob P = *Pp;
+    const int mx = P.m[0], my = P.m[1];
+    const int64_t nrows = r1 - r0;
     /* row pointers (sequential prefix sum) */
     rowptr[0] = 0;
-    for (int64_t r = 0; r < nrows; ++r) {
+    for (int64_t rr = 0; rr < nrows; ++rr) {
+        const int64_t r = r0 + rr;
         int ix = (int)(r % mx) + P.lo[0], iy = (int)((r / mx) % my) + P.lo[1], iz = (int)(r / ((int64_t)mx * my)) + P.lo[2];
         int lo[3], w[3];
-        rowptr[r + 1] = rowptr[r] + orc_row_cols(&P, ix, iy, iz, lo, w);
+        rowptr[rr + 1] = rowptr[rr] + orc_row_cols(&P, ix, iy, iz, lo, w);
     }
     const int px = P.T[0].p, py = P.T[1].p, pz = P.T[2].p;
     const int nqq = nq;
 #pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t r = 0; r < nrows; ++r) {
+    for (int64_t rr = 0; rr < nrows; ++rr) {
+        const int64_t r = r0 + rr;
         int ix = (int)(r % mx) + P.lo[0], iy = (int)((r / mx) % my) + P.lo[1], iz = (int)(r / ((int64_t)mx * my)) + P.lo[2];
         int lo[3], w[3];
         int64_t ncol = orc_row_cols(&P, ix, iy, iz, lo, w);
-        int64_t base = rowptr[r];
+        int64_t base = rowptr[rr];
         for (int64_t c = 0; c < ncol; ++c) {
             int jx = lo[0] + (int)(c % w[0]), jy = lo[1] + (int)((c / w[0]) % w[1]), jz = lo[2] + (int)(c / ((int64_t)w[0] * w[1]));
             colidx[base + c] = (int32_t)((((int64_t)(jz - P.lo[2]) * my) + (jy - P.lo[1])) * mx + (jx - P.lo[0]));
@@ -445,9 +447,60 @@ int orc_assemble_csr(const int* n, const int* p, const double* kx, const double*
                             }
                 }
     }
-    orc_prob_free(&P);
     return 0;
 }
+
+int orc_assemble_csr(const int* n, const int* p, const double* kx, const double* ky, const double* kz,
+                     int nq, int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
+                     int dirichlet, const double* w3, int64_t* rowptr, int32_t* colidx, double* valM, double* valS) {
+    return orc_assemble_csr_rows(n, p, kx, ky, kz, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3, 0, -1, rowptr,
+                                 colidx, valM, valS);
+}
+
+/* the same assembly restricted to the rows [r0, r1) (r1 < 0: all rows); rowptr has r1-r0+1
+   entries starting at 0.  Bench samples of full-size CSR (bench.py cpu_baseline). */
+int orc_assemble_csr_rows(const int* n, const int* p, const double* kx, const double* ky, const double* kz,
+                          int nq, int nt_m, const double* terms_m, const int* nt_q, const double* terms_q,
+                          int dirichlet, const double* w3, int64_t r0, int64_t r1, int64_t* rowptr, int32_t* colidx,
+                          double* valM, double* valS) {
+    const double* knots[3] = {kx, ky, kz};
+    orc_prob P;
+    if (orc_prob_build(&P, n, p, knots, nq, nt_m, terms_m, nt_q, terms_q, dirichlet, w3)) {
+        orc_prob_free(&P);
+        return 1;
+    }
+    const int64_t nrows = (int64_t)P.m[0] * P.m[1] * P.m[2];
+    if (r1 < 0) r1 = nrows;
+    int rc = 1;
+    if (r0 >= 0 && r0 <= r1 && r1 <= nrows) rc = orc_assemble_rows(&P, r0, r1, nq, rowptr, colidx, valM, valS);
+    orc_prob_free(&P);
+    return rc;
+}
+
+/* nnz of the rows [r0, r1) */
+int64_t orc_csr_rows_nnz(const int* n, const int* p, int dirichlet, int64_t r0, int64_t r1) {
+    const int lo = dirichlet ? 1 : 0;
+    const int m[3] = {n[0] - 2 * lo, n[1] - 2 * lo, n[2] - 2 * lo};
+    int64_t tot = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+        const int ii[3] = {(int)(r % m[0]) + lo, (int)((r / m[0]) % m[1]) + lo, (int)(r / ((int64_t)m[0] * m[1])) + lo};
+        int64_t c = 1;
+        for (int d = 0; d < 3; ++d) {
+            const int hi = n[d] - 1 - lo;
+            int a = ii[d] - p[d], b = ii[d] + p[d];
+            if (a < lo) a = lo;
+            if (b > hi) b = hi;
+            c *= b - a + 1;
+        }
+        tot += c;
+    }
+    return tot;
+}
+
+/* OpenMP threads of the oracle's parallel loops (bench: 1 thread vs all cores) */
+#include <omp.h>
+void orc_set_threads(int t) { omp_set_num_threads(t > 0 ? t : omp_get_num_procs()); }
+int orc_get_threads(void) { return omp_get_max_threads(); }
 
 /* naive CSR SpMV, y = A x; rows independent */
 int orc_spmv(int64_t nrows, const int64_t* rowptr, const int32_t* colidx, const double* val, const double* x,

@@ -657,3 +657,19 @@ def test_kkt_rows_matches_full_nonsym():
     samp = oracle.kkt_rows(P, X, cfg.tau, cfg.beta, steps, rows)
     for j, k in enumerate(steps):
         assert np.abs(samp[:, j] - full[:, k][:, rows]).max() < 1e-13 * np.abs(full).max()
+
+
+def test_csr_row_range_assembly_matches_full():
+    """P12-style self-consistency: the row-range assembly (bench samples of full-size CSR) is the
+    full assembly's rows, entry for entry, including Dirichlet problems."""
+    for dirichlet in (False, True):
+        cfg = synth.Config(95, "rows", n=9, p=3, R=2, batch=1, dirichlet=dirichlet)
+        w = synth.draw_weights(cfg, np.random.default_rng(9))
+        P = oracle.problem_from_config(cfg, w)
+        M, S = oracle.assemble_csr(P)
+        N = P.ndof
+        for r0, r1 in [(0, 7), (N // 3, N // 3 + 50), (N - 13, N), (0, N)]:
+            Mr, Sr = oracle.assemble_csr_rows(P, r0, r1)
+            assert (abs(Mr - M[r0:r1]).max() == 0.0) and (abs(Sr - S[r0:r1]).max() == 0.0)
+            x = np.random.default_rng(r0).standard_normal(N)
+            assert np.array_equal(oracle.spmv(Sr, x), oracle.spmv(S, x)[r0:r1])
