@@ -36,7 +36,13 @@ GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]EEEv")
 _MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dEEEvNS0_5Args2ENS0_6KSplitE"
 KNOWN_SPILLS = {
     _MK % ("11ShapeStiffA", 3, 16, 2, 1): (12, 20),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0): (12, 28),
+    # round 2 (tap-major p = 3 Y stage): narrow-tile (QX = 1, 2) variants, which no BASELINE mesh uses
+    _MK % ("11ShapeStiffA", 3, 16, 1, 0): (12, 28),
+    _MK % ("11ShapeStiffA", 3, 16, 1, 1): (20, 40),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0): (20, 40),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0): (12, 16),
+    _MK % ("11ShapeStiffA", 4, 12, 1, 0): (28, 52),
+    _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0): (68, 88),
     _MK % ("10ShapeMassKILi4EE", 3, 12, 2, 0): (76, 96),
     _MK % ("11ShapeStiffA", 4, 13, 4, 0): (56, 72),
     _MK % ("10ShapeMassKILi4EE", 4, 12, 1, 0): (32, 32),
@@ -44,7 +50,6 @@ KNOWN_SPILLS = {
     _MK % ("10ShapeMassKILi4EE", 4, 12, 4, 0): (100, 100),
     _MK % ("10ShapeMassKILi4EE", 4, 13, 4, 0): (92, 92),
     _MK % ("10ShapeMassKILi3EE", 4, 12, 2, 0): (64, 84),
-    _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0): (68, 84),
 }
 
 

@@ -32,6 +32,9 @@
 #ifndef IGALR_ZSMEM_P
 #define IGALR_ZSMEM_P 4  // (experiment knob: smallest degree whose stiffness kernel reads z from smem)
 #endif
+#ifndef IGALR_YTAP
+#define IGALR_YTAP 1  // 1: tap-major Y stage for p = 3 (YPitch::TAP); 0: factor-major everywhere
+#endif
 
 namespace igalr {
 namespace f2 {
@@ -579,6 +582,12 @@ struct ShapeStiffA {
         return (j == 0 || j == 1 || j == 3 || j == 4) ? 0 : (j == 2 || j == 5) ? 1 : (j == 6 || j == 7) ? 2 : 3;
     }
     __host__ __device__ static constexpr bool lead(int j) { return j == 0 || j == 2 || j == 6 || j == 8; }
+    // tap-major Y-stage issue order: consecutive pairs share their y-coefficient or their window
+    // value (M:K, M:E | T:E, T:M | M:M, M:T | E:T, E:M | K:M), so every DFMA but the first of a
+    // tap can take one operand from the operand-reuse cache
+    __host__ __device__ static constexpr int ord(int i) {
+        return i == 0 ? 0 : i == 1 ? 2 : i == 2 ? 1 : i == 3 ? 7 : i == 4 ? 8 : i == 5 ? 6 : i == 6 ? 3 : i == 7 ? 5 : 4;
+    }
 };
 // Mass: K consecutive rank-one terms per sweep (independent pipelines sharing the input
 // loads and the ring).
@@ -589,6 +598,7 @@ struct ShapeMassK {
     __host__ __device__ static constexpr int py(int j) { return j; }
     __host__ __device__ static constexpr int pg(int j) { return j; }
     __host__ __device__ static constexpr bool lead(int) { return true; }
+    __host__ __device__ static constexpr int ord(int i) { return i; }
 };
 using ShapeMass = ShapeMassK<4>;
 
@@ -610,6 +620,17 @@ struct GeoC {
     // segments start 16-byte aligned in global and shared memory (bulk copies); even pitch
     static constexpr int PADL = P & 1;
     static constexpr int HXP = (HX + PADL + 1) & ~1;
+};
+// y-coefficient record of one tile row: tap-major [k][NYP] (TAP: the factors of one tap are
+// adjacent, so a tap's coefficients are one or two broadcast LDS.128 and all pairs' chains advance
+// together) or factor-major [NY][BWP].  TAP for p = 3 only: measured on B200, c3 -0.4 %, c4 -1.4 %;
+// at p = 4 the NPAIR live accumulators push the sweep into spills (c5 +2 %).
+template <int NY, int BW>
+struct YPitch {
+    static constexpr bool TAP = IGALR_YTAP && BW == 7;
+    static constexpr int NYP = (NY + 1) & ~1;
+    static constexpr int BWP = (BW + 1) & ~1;
+    static constexpr int ROW = TAP ? BW * NYP : NY * BWP;  // doubles per tile row
 };
 template <int NG, int BW>
 struct ZPitch {
@@ -644,9 +665,11 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     // y-coefficients: all rounds resident per segment (YRES) or double-buffered per round
     constexpr int YSLOTS = YRES ? 0 : 2;
     const int nyslots = YRES ? a.nrounds : YSLOTS;
-    double* ycs = xcs + 2 * NX * TX * BW;               // [nyslots][NY][TY][BWP]
+    using YP = YPitch<NY, BW>;
+    constexpr int NYP = YP::NYP, YROW = YP::ROW;
+    double* ycs = xcs + 2 * NX * TX * BW;               // [nyslots][TY][YROW]
     constexpr int NGB = ZPitch<NG, BW>::NGB;
-    double* zcs = ycs + (size_t)nyslots * NY * TY * BWP;  // [2][nrounds][NGB] (per plane)
+    double* zcs = ycs + (size_t)nyslots * TY * YROW;    // [2][nrounds][NGB] (per plane)
     RoundT* rs = reinterpret_cast<RoundT*>(zcs + 2 * a.nrounds * NGB);
     __shared__ uint32_t tmem_base_sh;
     // bulk-copy completion of the x-coefficient buffers, per column group (GSYNC) or CTA-wide
@@ -672,6 +695,32 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     constexpr int GTHREADS = GSYNC ? 32 * WPQ * (4 / QX) : NW * WPQ * 32;
     const bool gprod = GSYNC ? (warp == grp && lane == 0) : (threadIdx.x == 0);  // x-copy issuer
     const int row0 = ((quad / QX) * WPQ + sub) * LW;          // first tile output row of this warp
+#ifdef IGALR_EXP_NOZ
+    double exp_sink = 0.0;
+#endif
+#ifdef IGALR_EXP_TIMERS
+    // experiment: per-warp cycle accounting of the round loop (sync, coefficient loads, sweep, retire)
+    long long exp_t[5] = {0, 0, 0, 0, 0}, exp_acc[4] = {0, 0, 0, 0};
+    const long long exp_t_start = clock64();
+#define EXP_T(k)                                                        \
+    do {                                                                \
+        exp_t[k] = clock64();                                           \
+        if ((k) > 0) exp_acc[(k) - 1] += exp_t[k] - exp_t[(k) - 1];     \
+    } while (0)
+#else
+#define EXP_T(k) do {} while (0)
+#endif
+    // y-coefficient rows of the tile for one round: [TY][YROW], entry (row, factor f, tap k) at
+    // k * NYP + f (YTAP) or f * BWP + k; one warp per (factor, row), lane k < BW copies one tap
+    auto copy_yrows = [&](double* ydst, const RoundT& R, int y0_) {
+        if (lane < BW) {
+            for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
+                const int f = rr / TY, row = rr - f * TY;
+                const int o = YP::TAP ? lane * NYP + f : f * BWP + lane;
+                cp8(ydst + (size_t)row * YROW + o, a.by + ((size_t)R.yf[f] * a.my + y0_ + row) * BW + lane, true);
+            }
+        }
+    };
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -721,14 +770,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         }
         if constexpr (YRES) {
             for (int r = 0; r < a.nrounds; ++r) {
-                const RoundT& R = rs[r];
-                double* ydst = ycs + (size_t)r * NY * TY * BWP;
-                if (lane < BW) {
-                    for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
-                        const int f = rr / TY, row = rr - f * TY;
-                        cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
-                    }
-                }
+                copy_yrows(ycs + (size_t)r * TY * YROW, rs[r], y0);
             }
         }
         {
@@ -837,15 +879,9 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     for (int i = threadIdx.x; i < TX * BW; i += blockDim.x) cp8(dstp + e * TX * BW + i, src + i, true);
                 }
             }
-            // y rows re-pitched from BW to BWP (16-byte aligned) for LDS.128 broadcasts
+            // y rows re-pitched (16-byte aligned records) for LDS.128 broadcasts
             if (YRES) return;
-            double* ydst = ycs + buf * NY * TY * BWP;
-            if (lane < BW) {
-                for (int rr = warp; rr < NY * TY; rr += NW * WPQ) {
-                    const int f = rr / TY, row = rr - f * TY;
-                    cp8(ydst + (size_t)rr * BWP + lane, a.by + ((size_t)R.yf[f] * a.my + y0 + row) * BW + lane, true);
-                }
-            }
+            copy_yrows(ycs + (size_t)buf * TY * YROW, R, y0);
         };
 
         if constexpr (GSYNC && DIST) {
@@ -859,6 +895,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         for (int zp = za; zp < zb; ++zp) {
             for (int r = 0; r < a.nrounds; ++r) {
                 const bool last_round = (r == a.nrounds - 1);
+                EXP_T(0);
                 if constexpr (GSYNC) {
                     tm_wait_st();
                     if (r == 0) {  // new plane buffer: CTA barrier, then request plane z'+1
@@ -876,6 +913,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
                     mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
                     xph ^= 1u << xbuf;
+                    EXP_T(1);
                 } else {
                     if constexpr (TMA) {  // x-coefficients arrive by cp.async.bulk (mbarrier)
                         mbar_wait(&xbar[0][xbuf], (xph >> xbuf) & 1);
@@ -893,7 +931,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 const RoundT& R = rs[r];
                 const double* vt = vin + pbuf * VSZ + row0 * HXP + PADL + cx;
                 const double* xc = xcs + xbuf * NX * TX * BW;
-                const double* yc = ycs + (size_t)(YRES ? r : xbuf) * NY * TY * BWP + (size_t)row0 * BWP;
+                const double* yc = ycs + (size_t)(YRES ? r : xbuf) * TY * YROW + (size_t)row0 * YROW;
                 const double* zc = zcs + pbuf * a.nrounds * NGB + r * NGB;
                 double xr[NX][BW];
 #pragma unroll
@@ -936,6 +974,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 // X stage of sweep row `step` into window slot Q (compile-time)
                 auto xstage = [&](auto Qc, int step) {
                     constexpr int Q = decltype(Qc)::value;
+#ifdef IGALR_EXP_EMPTY
+                    w[0][Q] = vt[step * HXP] * xr[Q % NX][Q % BW];
+                    return;
+#endif
                     double v[BW];
 #pragma unroll
                     for (int k = 0; k < BW; ++k) v[k] = vt[step * HXP + k];
@@ -955,15 +997,49 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     // TMEM load in flight during the Y stage (p=3); p=4 issues it after the Y stage:
                     // its 18 registers would push the Y stage into spills
                     constexpr bool EARLY_RING = (P <= 3) || ZSMEM;
+#ifndef IGALR_EXP_NOZ
                     if constexpr (EARLY_RING) ring_issue<BW, TIGHTR>(tp, rr);
+#endif
                     double G[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) G[g] = 0.0;
-                    const double* ycr = yc + (size_t)i * BWP;
+                    const double* ycr = yc + (size_t)i * YROW;
+#ifdef IGALR_EXP_EMPTY
+                    G[0] = w[0][Q] * ycr[0];
+                    if (false)
+#endif
+                    if constexpr (YP::TAP) {
+                        // tap-major: all NPAIR chains advance together (NPAIR independent chains);
+                        // the NY coefficients of tap k are NYP/2 broadcast LDS.128
+                        double acc[NPAIR];
+#pragma unroll
+                        for (int k = 0; k < BW; ++k) {
+                            double yv[NYP];
+                            const double2* y2 = reinterpret_cast<const double2*>(ycr + k * NYP);
+#pragma unroll
+                            for (int h = 0; h < NYP / 2; ++h) {
+                                const double2 t2 = y2[h];
+                                yv[2 * h] = t2.x;
+                                yv[2 * h + 1] = t2.y;
+                            }
+#pragma unroll
+                            for (int ii = 0; ii < NPAIR; ++ii) {
+                                const int j = S::ord(ii);
+                                const double wv = w[S::px(j)][(Q + 1 + k) % BW];
+                                acc[j] = k == 0 ? yv[S::py(j)] * wv : fma(yv[S::py(j)], wv, acc[j]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < NPAIR; ++j)
+                            if (S::lead(j)) G[S::pg(j)] = acc[j];
+#pragma unroll
+                        for (int j = 0; j < NPAIR; ++j)
+                            if (!S::lead(j)) G[S::pg(j)] = fma((P <= 3 || ZSMEM) ? pc[j] : R.pc[j], acc[j], G[S::pg(j)]);
+                    } else {
 #pragma unroll
                     for (int f = 0; f < NY; ++f) {
                         double yv[BWP];
-                        const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * TY * BWP);
+                        const double2* y2 = reinterpret_cast<const double2*>(ycr + (size_t)f * BWP);
 #pragma unroll
                         for (int k = 0; k < BWP / 2; ++k) {  // broadcast LDS.128
                             const double2 t2 = y2[k];
@@ -988,8 +1064,15 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                             }
                         }
                     }
+                    }
                     double ring[RS::DBL];
+#ifndef IGALR_EXP_NOZ
                     if constexpr (!EARLY_RING) ring_issue<BW, TIGHTR>(tp, rr);
+#endif
+#ifdef IGALR_EXP_NOZ
+                    (void)rr; (void)ring; (void)tp;
+                    exp_sink = fma(G[0] + G[1], G[NG - 1] + zr[0][Q % BW], exp_sink);
+#else
                     ring_wait<BW, TIGHTR>(rr, ring);
 #pragma unroll
                     for (int g = 0; g < NG; ++g)
@@ -997,10 +1080,12 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                         for (int j = 0; j < BW; ++j)
                             ring[j] = fma(ZSMEM ? zc[g * BW + j] : zr[ZSMEM ? 0 : g][ZSMEM ? 0 : j], G[g], ring[j]);
                     ring_st<BW, TIGHTR>(tp, ring);
+#endif
                 };
                 constexpr int HYW = LW + 2 * P;        // rows swept by this warp
                 constexpr int NFULL = (HYW - BW) / BW;  // full blocks after block 0
                 constexpr int REM = (HYW - BW) % BW;
+                EXP_T(2);
                 // block 0: the first 2P rows only fill the window
                 static_for<0, BW>([&](auto Qc) {
                     constexpr int Q = decltype(Qc)::value;
@@ -1020,6 +1105,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     xstage(Qc, step);
                     yzstage(Qc, step - 2 * P);
                 });
+                EXP_T(3);
                 if (ret_valid) {
                     // plane zret is final: write it (or its partial) out and clear its slot.  The
                     // LW TMEM loads are issued in chunks of 8 with one wait per chunk (a load+wait per
@@ -1089,6 +1175,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                         }
                     }
                 }
+                EXP_T(4);
                 if (last_round) pbuf ^= 1;
                 xbuf ^= 1;
             }
@@ -1124,6 +1211,15 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             }
         }
     }
+#ifdef IGALR_EXP_NOZ
+    if (a.accumulate == 12345) a.dst[threadIdx.x] = exp_sink;
+#endif
+#ifdef IGALR_EXP_TIMERS
+    if (lane == 0 && (blockIdx.x % 37) == 0)
+        printf("EXPT cta %d warp %d total %lld sync %lld load %lld sweep %lld retire %lld\n", blockIdx.x, warp,
+               clock64() - exp_t_start, exp_acc[0], exp_acc[1], exp_acc[2], exp_acc[3]);
+#endif
+#undef EXP_T
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1136,7 +1232,7 @@ size_t smem_bytes_canon(int nrounds) {
     using G_ = GeoC<P, TXT, TYT>;  // (padded pitch; the TMA variant uses the dense pitch, <= this)
     const size_t ys = YRES ? (size_t)nrounds : 2;
     const size_t vsz = (G_::HY * G_::HXP + 15) & ~(size_t)15;
-    return sizeof(double) * (2 * vsz + 2 * S::NX * TXT * G_::BW + ys * S::NY * TYT * G_::BWP +
+    return sizeof(double) * (2 * vsz + 2 * S::NX * TXT * G_::BW + ys * TYT * YPitch<S::NY, G_::BW>::ROW +
                              2 * (size_t)nrounds * ZPitch<S::NG, G_::BW>::NGB) +
            sizeof(RoundC<S>) * nrounds + 64;
 }
@@ -1738,6 +1834,15 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     // the GSYNC path (TMA && YRES) also bulk-copies plane rows: 16-byte aligned input
     const bool tma = !op->knobs.no_tma && (op->m[0] % 2 == 0) && ((uintptr_t)src % 16 == 0) && pl.d_ztab;
     const bool yres = !force_off && yres_fits<S, P, QX, LW>(pl.canon_nrounds);
+#ifdef IGALR_EXP_FAST  // (experiment builds: the GSYNC variants only, fast compiles)
+    if (!(tma && yres)) return cudaErrorNotSupported;
+    if (sp.bsplit) {
+        if constexpr (P == 3 && std::is_same<S, f2::ShapeStiffA>::value)
+            return launch_canon_t<S, P, QX, true, true, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        return cudaErrorNotSupported;
+    }
+    return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+#else
     if (sp.bsplit) {
         // batch split (KKT stiffness): p = 3 stiffness on the GSYNC path only; otherwise the
         // caller falls back to one launch per segment
@@ -1757,6 +1862,7 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     }
     if (yres) return launch_canon_t<S, P, QX, true, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     return launch_canon_t<S, P, QX, false, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+#endif
 }
 
 }  // namespace
@@ -1778,9 +1884,14 @@ cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* 
     if constexpr (P == 4) {
         if (tc.lw == 13) return launch_canon_q<S, P, 4, 13>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
+#ifdef IGALR_EXP_FAST
+    if (tc.qx != 4) return cudaErrorNotSupported;
+    return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+#else
     if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+#endif
 }
 #define IGALR_CAT2(a, b) a##b
 #define IGALR_CAT(a, b) IGALR_CAT2(a, b)
