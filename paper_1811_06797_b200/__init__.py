@@ -45,7 +45,7 @@ MINRES_X0 = 0x100
 class _Knobs(ctypes.Structure):
     """iga_test_knobs (include/iga_lr_testing.h): test-only kernel-selection overrides."""
     _fields_ = [("force_generic", ctypes.c_int32), ("qx", ctypes.c_int32), ("minlen", ctypes.c_int32),
-                ("no_yres", ctypes.c_int32), ("no_tma", ctypes.c_int32)]
+                ("no_yres", ctypes.c_int32), ("no_tma", ctypes.c_int32), ("vpack", ctypes.c_int32)]
 
 
 class IgaError(RuntimeError):
@@ -126,6 +126,8 @@ _lib.iga_tt_interfaces.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_
 _lib.iga_tt_local_apply.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
                                     _P, _P]
 _lib.iga_lr_test_knobs.argtypes = [_P, ctypes.POINTER(_Knobs)]
+_lib.iga_lr_test_tile.argtypes = [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_int32)]
 _lib.iga_lr_export_factor.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _D, ctypes.POINTER(ctypes.c_int32),
                                       ctypes.POINTER(ctypes.c_int32)]
 
@@ -318,12 +320,19 @@ class LowRankOperator:
                 "stiff_symmetric": bool(i.stiff_symmetric), "f2_rounds_stiff": int(i.f2_rounds_stiff)}
 
     def _test_knobs(self, force_generic: bool = False, qx: int = 0, minlen: int = 0, no_yres: bool = False,
-                    no_tma: bool = False):
+                    no_tma: bool = False, vpack: int = 0):
         """TEST-ONLY: override this op's kernel selection (iga_lr_test_knobs); all defaults
         restore the product's own choices."""
-        k = _Knobs(int(bool(force_generic)), int(qx), int(minlen), int(bool(no_yres)), int(bool(no_tma)))
+        k = _Knobs(int(bool(force_generic)), int(qx), int(minlen), int(bool(no_yres)), int(bool(no_tma)),
+                   int(vpack))
         _check(_lib.iga_lr_test_knobs(self._h, ctypes.byref(k)))
         self.info = self._info()
+
+    def _test_tile(self, batch: int) -> Tuple[int, int, int]:
+        """TEST-ONLY: the canonical tile (qx, lw, vp) for a launch over `batch` vectors."""
+        q, lw, vp = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.iga_lr_test_tile(self._h, int(batch), ctypes.byref(q), ctypes.byref(lw), ctypes.byref(vp)))
+        return q.value, lw.value, vp.value
 
     def export_factor(self, d: int, fid: int) -> Tuple[np.ndarray, int, int]:
         m = self.dims[d]

@@ -30,26 +30,31 @@ SOURCES = ["abi.cu", "factors.cu", "apply_unfused.cu", "apply_fused.cu", "apply_
 # (Other variants - odd extents, per-round y staging - may spill a few bytes; they are reported.)
 SPILL_RE = re.compile(r"Registers are spilled to local memory in function '([^']+)', (\d+) bytes spill stores, "
                       r"(\d+) bytes spill loads")
-GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]EEEv")
-# Ratchet: guarded variants that spilled in the round-1 build, with their byte counts (stores,
-# loads).  Any other guarded spill, or growth of these, fails the build.
-_MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dEEEvNS0_5Args2ENS0_6KSplitE"
+GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]ELb[01]EEEv")
+# Ratchet: guarded variants (k_canon<Shape, P, LW, 2, QX, YRES=1, TMA=1, SPLIT, PACK>) that spill in
+# the current build, with their byte counts (stores, loads).  Any other guarded spill, or growth of
+# these, fails the build.  The BASELINE kernels: c3 stiffness/mass (P 3, LW 16, QX 4) spill nothing;
+# c4 (P 3, LW 12, QX 2, split / packed) nothing; c5 stiffness and mass (P 4, LW 13, QX 4) nothing.
+_MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dELb%dEEEvNS0_5Args2ENS0_6KSplitE"
 KNOWN_SPILLS = {
-    _MK % ("11ShapeStiffA", 3, 16, 2, 1): (12, 20),
-    # round 2 (tap-major p = 3 Y stage): narrow-tile (QX = 1, 2) variants, which no BASELINE mesh uses
-    _MK % ("11ShapeStiffA", 3, 16, 1, 0): (12, 28),
-    _MK % ("11ShapeStiffA", 3, 16, 1, 1): (20, 40),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0): (20, 40),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0): (12, 16),
-    _MK % ("11ShapeStiffA", 4, 12, 1, 0): (28, 52),
-    _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0): (68, 88),
-    _MK % ("10ShapeMassKILi4EE", 3, 12, 2, 0): (76, 96),
-    _MK % ("11ShapeStiffA", 4, 13, 4, 0): (56, 72),
-    _MK % ("10ShapeMassKILi4EE", 4, 12, 1, 0): (32, 32),
-    _MK % ("10ShapeMassKILi4EE", 4, 12, 2, 0): (108, 108),
-    _MK % ("10ShapeMassKILi4EE", 4, 12, 4, 0): (100, 100),
-    _MK % ("10ShapeMassKILi4EE", 4, 13, 4, 0): (92, 92),
-    _MK % ("10ShapeMassKILi3EE", 4, 12, 2, 0): (64, 84),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 0): (20, 40),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 1): (52, 72),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 0): (12, 16),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 1): (32, 44),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 4, 0, 1): (44, 60),
+    _MK % ("11ShapeStiffA", 3, 12, 2, 1, 0): (56, 76),
+    _MK % ("11ShapeStiffA", 3, 16, 1, 0, 1): (4, 4),
+    _MK % ("11ShapeStiffA", 3, 16, 2, 0, 1): (4, 4),
+    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 0): (44, 60),
+    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 1): (52, 72),
+    _MK % ("11ShapeStiffA", 3, 16, 4, 0, 1): (4, 4),
+    _MK % ("11ShapeStiffA", 3, 16, 4, 1, 1): (52, 72),
+    _MK % ("10ShapeMassKILi3EE", 4, 12, 2, 0, 0): (64, 80),
+    _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0, 0): (68, 88),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 1, 0, 0): (32, 32),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 2, 0, 0): (108, 108),
+    _MK % ("10ShapeMassKILi4EE", 4, 12, 4, 0, 0): (100, 100),
+    _MK % ("10ShapeMassKILi4EE", 4, 13, 4, 0, 0): (92, 92),
 }
 
 

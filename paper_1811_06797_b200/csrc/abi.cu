@@ -882,11 +882,26 @@ iga_status iga_lr_test_knobs(iga_lr_op* op, const iga_test_knobs* k) {
     if (!op || !k) return set_error(IGA_EINVAL, "NULL argument");
     if (k->qx != 0 && k->qx != 1 && k->qx != 2 && k->qx != 4) return set_error(IGA_EINVAL, "qx must be 0, 1, 2 or 4");
     if (k->minlen < 0) return set_error(IGA_EINVAL, "minlen < 0");
+    if (k->vpack < 0) return set_error(IGA_EINVAL, "vpack < 0");
     op->knobs.force_generic = k->force_generic != 0;
     op->knobs.qx = k->qx;
     op->knobs.minlen = k->minlen;
     op->knobs.no_yres = k->no_yres != 0;
     op->knobs.no_tma = k->no_tma != 0;
+    op->knobs.vpack = k->vpack;
+    return IGA_OK;
+}
+
+iga_status iga_lr_test_tile(const iga_lr_op* op, int32_t batch, int32_t* qx, int32_t* lw, int32_t* vp) {
+    g_err.clear();
+    if (!op || !qx || !lw || !vp) return set_error(IGA_EINVAL, "NULL argument");
+    if (batch < 1) return set_error(IGA_EINVAL, "batch < 1");
+    if (!fused2_supported(op)) return set_error(IGA_EUNSUPPORTED, "no canonical kernel for this degree");
+    int q = 0, l = 0, v = 0;
+    canon_tile_choice(op, batch, &q, &l, &v);
+    *qx = q;
+    *lw = l;
+    *vp = v;
     return IGA_OK;
 }
 

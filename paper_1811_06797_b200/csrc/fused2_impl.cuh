@@ -79,8 +79,14 @@ struct Args2 {
 // Batch split of a canonical launch (KKT): vectors b >= bsplit read src + b*vol + src_jump and
 // write dst + b*vol + dst_jump (element offsets).  A separate kernel parameter: growing Args2 moves
 // the register-tight p = 4 kernel over the spill cliff.
+// vp > 1 (GSYNC path only): vector packing along x.  A launch row is vp consecutive vectors' rows
+// side by side (width vp * mx); packed column c of vector group g belongs to vector g * vp + c / mx,
+// local column c % mx.  Seams need no gap: a factor's band row holds zeros for columns outside the
+// matrix, so the taps that cross a seam multiply by 0.  Narrow meshes then fill the 32-lane column
+// groups (46 columns: 72 % of a 64-wide tile; 4 packed vectors: 184 of 192 columns).
 struct KSplit {
     long long bsplit, src_jump, dst_jump;
+    int vp;
 };
 
 constexpr int NSEG = 4;    // max segments per CTA (checked on the host)
@@ -644,7 +650,7 @@ __host__ __device__ constexpr bool gsync_path() {
 }
 
 // QX of the 4 TMEM lane quadrants tile x (32 columns each); the other 4/QX stack in y.
-template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA, bool SPLIT = false>
+template <class S, int P, int LW, int WPQ, int QX, bool YRES, bool TMA, bool SPLIT = false, bool PACK = false>
 __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const KSplit ks) {
     constexpr int TX = 32 * QX;                 // tile columns (shadows the 128-wide default)
     constexpr int TY = LW * WPQ * (4 / QX);     // tile rows
@@ -756,10 +762,30 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         const int x0 = txi * TX, y0 = tyi * TY;
         // input / output vector bases; SPLIT (KKT): vectors b >= bsplit jump (a compile-time
         // variant, so the register-tight p = 4 kernels are untouched)
-        const long long vb = (long long)b * a.mz * plane;
-        const long long vbs = SPLIT ? vb + (b >= ks.bsplit ? ks.src_jump : 0) : vb;
-        const long long vbd = SPLIT ? vb + (b >= ks.bsplit ? ks.dst_jump : 0) : vb;
-        const int gx = x0 + cx;
+        // (b is the vector group: vectors b * vp .. b * vp + vp - 1, side by side along x)
+        // (PACK: a compile-time variant, so the unpacked production kernels are untouched)
+        const int VPK = (GSYNC && PACK) ? ks.vp : 1;
+        const int WX = VPK * a.mx;  // packed row width
+        auto vsrc = [&](int v) -> long long {
+            return (long long)v * a.mz * plane + (SPLIT && v >= ks.bsplit ? ks.src_jump : 0);
+        };
+        auto vdst = [&](int v) -> long long {
+            return (long long)v * a.mz * plane + (SPLIT && v >= ks.bsplit ? ks.dst_jump : 0);
+        };
+        const long long vbs = vsrc(b);  // (unpacked staging paths: VPK == 1)
+        const long long vbd = vdst(b);
+        const int gx = x0 + cx;          // packed column of this thread
+        // output column of this thread: vector, local column, validity (recomputed at plane retire)
+        auto out_col = [&](bool* ok) -> double* {
+            if constexpr (!PACK) {
+                *ok = gx < a.mx;
+                return a.dst + vbd + gx;
+            }
+            const int vi = min(gx / a.mx, VPK - 1);
+            const int vv = b * VPK + vi;
+            *ok = gx < WX && vv < a.batch;
+            return a.dst + vdst(vv) + (gx - vi * a.mx);
+        };
 
         __syncthreads();
         if constexpr (GSYNC) {
@@ -781,13 +807,28 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         }
 
         // GSYNC: the byte count of a plane's copies, registered by thread 0 before they are issued
+        // GSYNC plane rows: the packed column range [cs, ce) of the tile (halo included) in pieces of
+        // one vector each; f(vector, local column, packed column, count) for the existing vectors
+        auto plane_pieces = [&](auto&& f) {
+            const int cs = max(x0 - P - PADL, 0);
+            const int ce = min((min(x0 + TX + P, WX) + 1) & ~1, WX);
+            if constexpr (!PACK) {
+                f(b, cs, cs, ce - cs);
+                return;
+            }
+            for (int c = cs; c < ce;) {
+                const int vi = c / a.mx;
+                const int n = min(ce, (vi + 1) * a.mx) - c;
+                if (b * VPK + vi < a.batch) f(b * VPK + vi, c - vi * a.mx, c, n);
+                c += n;
+            }
+        };
         auto stage_plane_expect = [&](int buf) {
             if (threadIdx.x == 0) {
-                const int cbase = x0 - P - PADL;
-                const int cs = max(cbase, 0);
-                const int ce = min((min(x0 + TX + P, a.mx) + 1) & ~1, a.mx);
                 const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
-                const uint32_t rb = (uint32_t)((ce - cs) * sizeof(double));
+                int ncol = 0;
+                plane_pieces([&](int, int, int, int n) { ncol += n; });
+                const uint32_t rb = (uint32_t)(ncol * sizeof(double));
                 const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
                 mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
             }
@@ -804,14 +845,14 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 if (DIST ? lane == 0 : threadIdx.x == 0) {
                     if (!DIST) stage_plane_expect(buf);
                     const int cbase = x0 - P - PADL;
-                    const int cs = max(cbase, 0);
-                    const int ce = min((min(x0 + TX + P, a.mx) + 1) & ~1, a.mx);
                     const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
-                    const uint32_t rb = (uint32_t)((ce - cs) * sizeof(double));
-                    double* dstp = vin + buf * VSZ + (cs - cbase);
-                    const double* srcp = a.src + vbs + (long long)zp * plane + cs;
-                    for (int r = rlo + (DIST ? warp : 0); r < rhi; r += (DIST ? NW * WPQ : 1))
-                        bulk_g2s(dstp + r * HXP, srcp + (long long)(y0 - P + r) * a.mx, rb, &pbar[buf]);
+                    plane_pieces([&](int v, int lx, int c, int n) {
+                        double* dstp = vin + buf * VSZ + (c - cbase);
+                        const double* srcp = a.src + vsrc(v) + (long long)zp * plane + lx;
+                        for (int r = rlo + (DIST ? warp : 0); r < rhi; r += (DIST ? NW * WPQ : 1))
+                            bulk_g2s(dstp + r * HXP, srcp + (long long)(y0 - P + r) * a.mx,
+                                     (uint32_t)(n * sizeof(double)), &pbar[buf]);
+                    });
                     if (!DIST || warp == NW * WPQ - 1) {
                         const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
                         bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes,
@@ -858,11 +899,27 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 // the column group's 32 columns of every x-entry
                 if (gprod) {
                     mbar_expect_tx(&xbar[grp][buf], (uint32_t)(NX * TXW * BW * sizeof(double)));
+                    // packed columns [c0, c0 + 32) in pieces of one vector each (the band rows of the
+                    // local columns; columns past the packed width read the last vector's padding rows)
+                    if constexpr (!PACK) {
 #pragma unroll
-                    for (int e = 0; e < NX; ++e)
-                        bulk_g2s(dstp + e * TX * BW + grp * TXW * BW,
-                                 a.bx + ((size_t)R.xf[e] * a.mx + x0 + grp * TXW) * BW,
-                                 (uint32_t)(TXW * BW * sizeof(double)), &xbar[grp][buf]);
+                        for (int e = 0; e < NX; ++e)
+                            bulk_g2s(dstp + e * TX * BW + grp * TXW * BW,
+                                     a.bx + ((size_t)R.xf[e] * a.mx + x0 + grp * TXW) * BW,
+                                     (uint32_t)(TXW * BW * sizeof(double)), &xbar[grp][buf]);
+                        return;
+                    }
+                    const int c0 = x0 + grp * TXW;
+                    for (int c = c0; c < c0 + TXW;) {
+                        const int vi = min(c / a.mx, VPK - 1);
+                        const int n = (vi == VPK - 1 ? c0 + TXW : min(c0 + TXW, (vi + 1) * a.mx)) - c;
+#pragma unroll
+                        for (int e = 0; e < NX; ++e)
+                            bulk_g2s(dstp + e * TX * BW + (c - x0) * BW,
+                                     a.bx + ((size_t)R.xf[e] * a.mx + (c - vi * a.mx)) * BW,
+                                     (uint32_t)(n * BW * sizeof(double)), &xbar[grp][buf]);
+                        c += n;
+                    }
                 }
             } else if constexpr (TMA) {
                 if (threadIdx.x == 0) {
@@ -963,6 +1020,18 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                     ret_valid = true;
                     const int lo = max(0, zret - P), hi = min(a.mz - 1, zret + P);
                     ret_complete = lo >= za && hi <= zb - 1;
+                }
+                if (SPLIT && a.accumulate && r == max(0, a.nrounds - 2) && zret >= 0 && zret < a.mz &&
+                    max(0, zret - P) >= za && min(a.mz - 1, zret + P) <= zb - 1) {
+                    // the plane this step retires is read-modify-written: its rows go to L2 a round
+                    // ahead (an exposed HBM read per plane otherwise).  The KKT's accumulating
+                    // stiffness launch only (SPLIT): in the other kernels the extra code costs more
+                    // (register allocation) than the rare accumulate saves
+                    bool ok;
+                    const double* prow = out_col(&ok) + (long long)zret * plane + (long long)(y0 + row0) * a.mx;
+                    const int nrow = min(LW, a.my - (y0 + row0));
+                    if (ok)
+                        for (int i = 0; i < nrow; ++i) asm volatile("prefetch.global.L2 [%0];" ::"l"(prow + (long long)i * a.mx));
                 }
 
                 double w[NX][BW];
@@ -1138,9 +1207,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                         // stores: the plane-uniform cases (complete / partial, accumulate) are split
                         // outside the row loop, so each row is one predicated store (no per-row branches)
                         const int nrow = min(LW, a.my - (y0 + row0));  // rows of this warp inside the mesh
-                        const bool colok = gx < a.mx;
+                        bool colok;
+                        double* dcol = out_col(&colok);
                         if (ret_complete) {
-                            double* drow = a.dst + vbd + (long long)zret * plane + (long long)(y0 + row0) * a.mx + gx;
+                            double* drow = dcol + (long long)zret * plane + (long long)(y0 + row0) * a.mx;
                             if (a.accumulate) {
 #pragma unroll
                                 for (int i = 0; i < LW; ++i)
@@ -1158,14 +1228,16 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                                 if (colok && i < nrow) srow[(size_t)i * TX] = a.scale * rv[i];
                         }
                     } else {
+                        bool colok;
+                        double* dcol = out_col(&colok);
 #pragma unroll
                         for (int i = 0; i < LW; ++i) {
                             const double val = rv[i];
                             const int gy = y0 + row0 + i;
-                            if (gy < a.my && gx < a.mx) {
+                            if (gy < a.my && colok) {
                                 if (ret_complete) {
-                                    const long long o = vbd + (long long)zret * plane + (long long)gy * a.mx + gx;
-                                    a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                                    double* o = dcol + (long long)zret * plane + (long long)gy * a.mx;
+                                    *o = (a.accumulate ? *o : 0.0) + a.scale * val;
                                 } else {
                                     const int slot = partial_slot(zret, za, zb, P);
                                     a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
@@ -1182,6 +1254,8 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         }
         tm_wait_st();
         __syncthreads();
+        bool fcolok;
+        double* fdcol = out_col(&fcolok);
         for (int i = 0; i < LW; ++i) {
             const uint32_t tp = tbase + i * RS::COLS;
             double ring[RS::DBL];
@@ -1196,12 +1270,12 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #pragma unroll
                 for (int jj = 0; jj < BW; ++jj)
                     if (jj == j) val = ring[jj];
-                if (gy < a.my && gx < a.mx) {
+                if (gy < a.my && fcolok) {
                     const int lo = max(0, zo - P), hi = min(a.mz - 1, zo + P);
                     const bool complete = lo >= za && hi <= zb - 1;
                     if (complete) {
-                        const long long o = vbd + (long long)zo * plane + (long long)gy * a.mx + gx;
-                        a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + a.scale * val;
+                        double* o = fdcol + (long long)zo * plane + (long long)gy * a.mx;
+                        *o = (a.accumulate ? *o : 0.0) + a.scale * val;
                     } else {
                         const int slot = partial_slot(zo, za, zb, P);
                         a.scratch[((((size_t)blockIdx.x * NSEG + seg) * 4 * P + slot) * TY + row0 + i) * TX + cx] =
@@ -1310,7 +1384,15 @@ static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const F
     const FixEnt& E = tab[blockIdx.x];
     const int TY = a.tyt, TX = a.txt;
     const long long plane = (long long)a.mx * a.my;
-    const long long obase = (long long)E.b * a.mz * plane + (long long)E.zo * plane + (E.b >= ks.bsplit ? ks.dst_jump : 0);
+    const int WX = ks.vp * a.mx;  // packed row width (E.b is the vector group)
+    // element offset of packed column gx in row gy of plane E.zo, or -1 outside the vectors
+    auto out_off = [&](int gx, int gy) -> long long {
+        const int vi = min(gx / a.mx, ks.vp - 1);
+        const int vv = E.b * ks.vp + vi;
+        if (gx >= WX || vv >= a.batch) return -1;
+        return (long long)vv * a.mz * plane + (vv >= ks.bsplit ? ks.dst_jump : 0) + (long long)E.zo * plane +
+               (long long)gy * a.mx + (gx - vi * a.mx);
+    };
     const int n = E.n;
     const int nq = TY * TX / 4;
     for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * blockDim.x) {
@@ -1347,8 +1429,10 @@ static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const F
             const int gy = E.tyi * TY + i;
             if (gy >= a.my) continue;
             const int gx0 = E.txi * TX + cx;
-            const long long o0 = obase + (long long)gy * a.mx + gx0;
-            if (gx0 + 3 < a.mx && ((uintptr_t)(a.dst + o0) & 31) == 0) {  // whole aligned quad: one 32-byte access
+            const long long o0 = out_off(gx0, gy);
+            const int lx0 = gx0 - min(gx0 / a.mx, ks.vp - 1) * a.mx;
+            // whole aligned quad inside one vector: one 32-byte access
+            if (o0 >= 0 && lx0 + 3 < a.mx && ((uintptr_t)(a.dst + o0) & 31) == 0) {
                 double4* d4 = reinterpret_cast<double4*>(a.dst + o0);
                 double4 r = acc[t];
                 if (a.accumulate) {
@@ -1364,9 +1448,8 @@ static __global__ void __launch_bounds__(256) k_fixup_tab(const Args2 a, const F
             const double vv[4] = {acc[t].x, acc[t].y, acc[t].z, acc[t].w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-                const int gx = gx0 + w;
-                if (gx >= a.mx) continue;
-                const long long o = obase + (long long)gy * a.mx + gx;
+                const long long o = out_off(gx0 + w, gy);
+                if (o < 0) continue;
                 a.dst[o] = (a.accumulate ? a.dst[o] : 0.0) + vv[w];
             }
         }
@@ -1636,27 +1719,52 @@ struct CanonCfg {
 // badly (e.g. 46 interior rows: 48-row tiles instead of 64).  Cost = padded area x the X stage's
 // y-halo recompute (the X stage is ~1/5 of a point's FP64 work).  Ties -> the first candidate.
 struct TileChoice {
-    int qx, lw;
+    int qx, lw, vp;  // vp: vectors packed along x (GSYNC path; KSplit::vp)
 };
-static TileChoice pick_tile(int mx, int my, int P, int qx_override = 0) {
+// columns of a tile row holding packed vector data / columns covered, for vp vectors of width mx
+static double pack_util(int mx, int tx, int vp) {
+    const long long w = (long long)vp * mx;
+    return (double)w / (double)((w + tx - 1) / tx * tx);
+}
+static TileChoice pick_tile(int mx, int my, int P, int batch = 1, int qx_override = 0, int vp_override = 0) {
     const int LW0 = P == 3 ? CanonCfg<3>::LW : CanonCfg<4>::LW;
     // p = 3 also weighs 48-row tiles (LW 12, QX 2); p = 4 weighs LW 13 (26-row tiles, 234 of a
     // warp's 256 TMEM columns with the 9-double ring): 256 rows tile as 10 x 26 instead of 11 x 24
-    TileChoice cand[4] = {{4, LW0}, {2, LW0}, {1, LW0}, {P == 3 ? 2 : 4, P == 3 ? 12 : 13}};
+    TileChoice cand[4] = {{4, LW0, 1}, {2, LW0, 1}, {1, LW0, 1}, {P == 3 ? 2 : 4, P == 3 ? 12 : 13, 1}};
     const int ncand = 4;
     TileChoice best = cand[0];
     double bc = 1e30;
     for (int i = 0; i < ncand; ++i) {
         const int tx = 32 * cand[i].qx, ty = cand[i].lw * 2 * (4 / cand[i].qx);
-        const double waste = (double)((mx + tx - 1) / tx * tx) / mx * (double)((my + ty - 1) / ty * ty) / my;
+        // vectors per packed row: the smallest count with the best column utilisation (a batch of
+        // narrow vectors fills the tile columns; one vector per row when the mesh is wide enough)
+        int vp = 1;
+        double ux = pack_util(mx, tx, 1);
+        for (int v = 2; v <= std::min(batch, 32) && (long long)(v - 1) * mx < 4LL * tx; ++v)
+            if (pack_util(mx, tx, v) > ux + 0.02) {
+                ux = pack_util(mx, tx, v);
+                vp = v;
+            }
+        if (vp_override > 0) {
+            vp = std::min(vp_override, std::max(batch, 1));
+            ux = pack_util(mx, tx, vp);
+        }
+        // (a packed tile row costs more staging copies and a wider fixup mapping: only worth it
+        // when the columns are used clearly better)
+        if (vp > 1 && vp_override <= 0) ux /= 1.03;
+        const double waste = 1.0 / ux * (double)((my + ty - 1) / ty * ty) / my;
         const double halo = (double)(cand[i].lw + 2 * P) / cand[i].lw;
         const double cost = waste * (0.8 + 0.2 * halo);
         if (cost < bc - 1e-9) {
             bc = cost;
             best = cand[i];
+            best.vp = vp;
         }
     }
-    if (qx_override == 1 || qx_override == 2 || qx_override == 4) best = {qx_override, LW0};  // (test knob)
+    if (qx_override == 1 || qx_override == 2 || qx_override == 4) {  // (test knob)
+        best = {qx_override, LW0, 1};
+        if (vp_override > 0) best.vp = std::min(vp_override, std::max(batch, 1));
+    }
     return best;
 }
 
@@ -1671,12 +1779,12 @@ static long long canon_minlen(const iga_lr_op* op, long long units, int P, int s
 // [za, zb) writes every zo in [za-P, zb+P) of the mesh, to scratch slot partial_slot(zo, za, zb, P)
 // unless all of zo's input planes [zo-P, zo+P] lie in [za, zb)).  Built once per launch shape and
 // cached in the op (device copy); deterministic.
-static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, const f2::FixEnt** tab, int* n,
+static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, int vp, const f2::FixEnt** tab, int* n,
                                cudaStream_t st) {
-    const long long key[9] = {P, a.tyt, a.txt, a.tiles_x, a.tiles_y, a.batch, a.mx, a.my, a.nctas};
+    const long long key[10] = {P, a.tyt, a.txt, a.tiles_x, a.tiles_y, a.batch, a.mx, a.my, a.nctas, vp};
     std::lock_guard<std::mutex> lock(op->fix_mu);
     for (const auto& c : op->fix_cache)
-        if (std::equal(key, key + 9, c.key)) {
+        if (std::equal(key, key + 10, c.key)) {
             *tab = static_cast<const f2::FixEnt*>(c.d_tab);
             *n = c.n;
             // the upload may have been queued on another stream: order this launch after it
@@ -1712,7 +1820,7 @@ static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, c
     v.reserve(ents.size());
     for (auto& kv : ents) v.push_back(kv.second);
     iga_lr_op::FixCache c;
-    std::copy(key, key + 9, c.key);
+    std::copy(key, key + 10, c.key);
     c.n = (int)v.size();
     c.d_tab = nullptr;
     c.ready = nullptr;
@@ -1735,7 +1843,7 @@ static cudaError_t fixup_table(const iga_lr_op* op, const f2::Args2& a, int P, c
     return cudaSuccess;
 }
 
-template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW, bool SPLIT = false>
+template <class S, int P, int QX, bool YRES, bool TMA, int LW = CanonCfg<P>::LW, bool SPLIT = false, bool PACK = false>
 cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                            int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     using namespace f2;
@@ -1757,11 +1865,14 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     a.my = op->m[1];
     a.mz = op->m[2];
     a.batch = batch;
-    a.tiles_x = (a.mx + TXT - 1) / TXT;
+    // vector packing along x: the GSYNC path only (bulk-copied rows, one piece per vector)
+    const int vp = PACK ? std::max(1, std::min(sp.vp, batch)) : 1;
+    const int groups = (batch + vp - 1) / vp;
+    a.tiles_x = (vp * a.mx + TXT - 1) / TXT;
     a.tiles_y = (a.my + TYT - 1) / TYT;
     a.txt = TXT;
     a.tyt = TYT;
-    a.units = (long long)a.tiles_x * a.tiles_y * batch * a.mz;
+    a.units = (long long)a.tiles_x * a.tiles_y * groups * a.mz;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1775,11 +1886,12 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
     a.nctas = (int)nct;
     const size_t sm = smem_bytes_canon<S, P, LW, WPQ, QX, YRES>(a.nrounds);
-    auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA, SPLIT>;
+    auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA, SPLIT, PACK>;
     f2::KSplit ks;
     ks.bsplit = sp.bsplit;
     ks.src_jump = sp.src_jump;
     ks.dst_jump = sp.dst_jump;
+    ks.vp = vp;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
     const size_t scratch_elems = (size_t)a.nctas * NSEG * 4 * P * TYT * TXT;
@@ -1788,7 +1900,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     int nfix = 0;
     const f2::FixEnt* tab = nullptr;
     if (a.nctas > 1) {
-        e = fixup_table(op, a, P, &tab, &nfix, st);
+        e = fixup_table(op, a, P, vp, &tab, &nfix, st);
         if (e) {
             cudaFreeAsync(a.scratch, st);
             return e;
@@ -1802,6 +1914,18 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     }
     cudaFreeAsync(a.scratch, st);
     return e;
+}
+
+// GSYNC launch; vector packing (sp.vp > 1) has its own kernel variant, for p = 3 (p = 4 sits at the
+// register cliff)
+template <class S, int P, int QX, int LW, bool SPLIT>
+cudaError_t launch_gsync(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
+                         int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
+    if constexpr (P == 3) {
+        if (sp.vp > 1 && batch > 1)
+            return launch_canon_t<S, P, QX, true, true, LW, SPLIT, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    }
+    return launch_canon_t<S, P, QX, true, true, LW, SPLIT>(op, pl, src, dst, scale, accumulate, batch, st, sp);
 }
 
 template <class S, int P, int QX, int LW = CanonCfg<P>::LW>
@@ -1838,26 +1962,26 @@ cudaError_t launch_canon_q(const iga_lr_op* op, const Plan& pl, const double* sr
     if (!(tma && yres)) return cudaErrorNotSupported;
     if (sp.bsplit) {
         if constexpr (P == 3 && std::is_same<S, f2::ShapeStiffA>::value)
-            return launch_canon_t<S, P, QX, true, true, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+            return launch_gsync<S, P, QX, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
         return cudaErrorNotSupported;
     }
-    return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+    return launch_gsync<S, P, QX, LW, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
 #else
     if (sp.bsplit) {
         // batch split (KKT stiffness): p = 3 stiffness on the GSYNC path only; otherwise the
         // caller falls back to one launch per segment
         if constexpr (P == 3 && std::is_same<S, f2::ShapeStiffA>::value) {
-            if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+            if (tma && yres) return launch_gsync<S, P, QX, LW, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
         }
         return cudaErrorNotSupported;
     }
     if constexpr (LW != CanonCfg<P>::LW) {
         // alternative row count: instantiated for the GSYNC path only
-        if (tma && yres) return launch_canon_t<S, P, QX, true, true, LW>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        if (tma && yres) return launch_gsync<S, P, QX, LW, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
         return launch_canon_q<S, P, QX>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
     if (tma) {
-        if (yres) return launch_canon_t<S, P, QX, true, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
+        if (yres) return launch_gsync<S, P, QX, CanonCfg<P>::LW, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
         return launch_canon_t<S, P, QX, false, true>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
     if (yres) return launch_canon_t<S, P, QX, true, false>(op, pl, src, dst, scale, accumulate, batch, st, sp);
@@ -1875,23 +1999,28 @@ cudaError_t canon_launch_p4(int part, const iga_lr_op* op, const Plan& pl, const
 
 #if defined(IGALR_CANON_P) && IGALR_CANON_P != 99  // (99: experiment TUs instantiate kernels themselves)
 template <class S, int P>
+cudaError_t launch_canon_tile(const TileChoice& tc, const iga_lr_op* op, const Plan& pl, const double* src, double* dst,
+                              double scale, int accumulate, int batch, cudaStream_t st, const CanonSplit& sp);
+template <class S, int P>
 cudaError_t launch_canon_deg(const iga_lr_op* op, const Plan& pl, const double* src, double* dst, double scale,
                              int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
-    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, op->knobs.qx);
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, batch, op->knobs.qx, op->knobs.vpack);
+    CanonSplit spv = sp;
+    spv.vp = tc.vp;
+    return launch_canon_tile<S, P>(tc, op, pl, src, dst, scale, accumulate, batch, st, spv);
+}
+template <class S, int P>
+cudaError_t launch_canon_tile(const TileChoice& tc, const iga_lr_op* op, const Plan& pl, const double* src, double* dst,
+                              double scale, int accumulate, int batch, cudaStream_t st, const CanonSplit& sp) {
     if constexpr (P == 3) {
         if (tc.lw == 12) return launch_canon_q<S, P, 2, 12>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
     if constexpr (P == 4) {
         if (tc.lw == 13) return launch_canon_q<S, P, 4, 13>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     }
-#ifdef IGALR_EXP_FAST
-    if (tc.qx != 4) return cudaErrorNotSupported;
-    return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
-#else
     if (tc.qx == 4) return launch_canon_q<S, P, 4>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     if (tc.qx == 2) return launch_canon_q<S, P, 2>(op, pl, src, dst, scale, accumulate, batch, st, sp);
     return launch_canon_q<S, P, 1>(op, pl, src, dst, scale, accumulate, batch, st, sp);
-#endif
 }
 #define IGALR_CAT2(a, b) a##b
 #define IGALR_CAT(a, b) IGALR_CAT2(a, b)
@@ -2009,13 +2138,22 @@ bool canon_small_grid(const iga_lr_op* op, int batch) {
     // both parts' persistent grids fit the GPU side by side: launch them concurrently
     if (!fused2_supported(op)) return false;
     const int P = op->p[0];
-    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, op->knobs.qx);
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], P, batch, op->knobs.qx, op->knobs.vpack);
     const long long tx = 32 * tc.qx, ty = (long long)tc.lw * 2 * (4 / tc.qx);
-    const long long units = (op->m[0] + tx - 1) / tx * ((op->m[1] + ty - 1) / ty) * batch * op->m[2];
+    const long long vp = op->m[0] % 2 == 0 ? tc.vp : 1;  // (packing needs the bulk-copy path: even nx)
+    const long long units =
+        (vp * op->m[0] + tx - 1) / tx * ((op->m[1] + ty - 1) / ty) * ((batch + vp - 1) / vp) * op->m[2];
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return 2 * units <= sms;
+}
+
+void canon_tile_choice(const iga_lr_op* op, int batch, int* qx, int* lw, int* vp) {
+    const TileChoice tc = pick_tile(op->m[0], op->m[1], op->p[0], batch, op->knobs.qx, op->knobs.vpack);
+    *qx = tc.qx;
+    *lw = tc.lw;
+    *vp = op->p[0] == 3 && op->m[0] % 2 == 0 ? std::min(tc.vp, std::max(batch, 1)) : 1;  // (launch_gsync)
 }
 
 bool fused2_preferred(const iga_lr_op* op, int batch) {

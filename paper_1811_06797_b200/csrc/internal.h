@@ -125,6 +125,7 @@ struct iga_lr_op {
         int minlen = 0;         // > 0: persistent-CTA range length in planes
         int no_yres = 0;        // 1: per-round y-coefficient staging
         int no_tma = 0;         // 1: no bulk-copy staging
+        int vpack = 0;          // > 0: vectors packed along x per canonical tile row (1: no packing)
     } knobs;
     igalr::DirFactors F[3];
     igalr::DirQuad quad[3];   // (kept for derived operators: the KKT preconditioner)
@@ -134,7 +135,7 @@ struct iga_lr_op {
     std::vector<igalr::KTerm> kterms;  // merged term list, r-major (NEXT-3 TT functions)
     // fixup tables of the canonical kernels, per launch shape (built on first use; fused2_impl.cuh)
     struct FixCache {
-        long long key[9];
+        long long key[10];  // launch shape (fixup_table)
         void* d_tab;
         int n;
         cudaEvent_t ready;  // recorded after the table's upload; every user waits on it
@@ -184,12 +185,16 @@ void release_fused(Plan* pl);
 bool fused2_supported(const iga_lr_op* op);
 bool fused2_preferred(const iga_lr_op* op, int batch);
 bool canon_small_grid(const iga_lr_op* op, int batch);
+// canonical tile of a launch over `batch` vectors: 32*qx columns, 2*lw*(4/qx) rows, vp vectors
+// packed along x (the packed variant exists for p = 3 on the bulk-copy path)
+void canon_tile_choice(const iga_lr_op* op, int batch, int* qx, int* lw, int* vp);
 iga_status prepare_fused2(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st);
 iga_status prepare_canon(const iga_lr_op* op, Plan* pl, int part, cudaStream_t st);
 // Batch split of a canonical launch (KKT): vectors b >= bsplit are read at src + b*vol + src_jump
 // and written at dst + b*vol + dst_jump (element offsets).  The default is the plain batch.
 struct CanonSplit {
     long long bsplit = 0, src_jump = 0, dst_jump = 0;
+    int vp = 1;  // vectors packed along x (set by the tile choice; the GSYNC path only)
 };
 iga_status apply_canon_part(const iga_lr_op* op, const Plan& pl, int part, const double* src, double* dst, double scale,
                             int accumulate, int batch, cudaStream_t st, const CanonSplit& sp = CanonSplit());

@@ -38,8 +38,9 @@ def test_testing_header_symbols_exported(igalr):
     product binding no longer takes its library path from the environment."""
     lib = ctypes.CDLL(igalr.LIB_PATH)
     names = _declared_symbols("iga_lr_testing.h")
-    assert names == ["iga_lr_test_knobs"]
-    assert hasattr(lib, "iga_lr_test_knobs")
+    assert names == ["iga_lr_test_knobs", "iga_lr_test_tile"]
+    for n in names:
+        assert hasattr(lib, n), "missing export " + n
     assert igalr.LIB_PATH == os.path.join(ROOT, "paper_1811_06797_b200", "libigalr.so")
     src = open(os.path.join(ROOT, "paper_1811_06797_b200", "__init__.py")).read()
     assert "environ" not in src

@@ -44,8 +44,7 @@ def test_weak_scaling_aggregation_gloo_ws2():
 
 def test_reference_arm_json_contract():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--cpu-seconds", "0.6", "--config", "c2"], capture_output=True, text=True, timeout=600,
-                         cwd=ROOT)
+                          "--warmup", "1", "--config", "c2"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)

@@ -303,3 +303,72 @@ def test_binding_rejects_undersized_buffers(env):
     op.apply(x, torch.empty_like(x), torch.empty_like(x))
     op.kkt_apply(X, torch.empty_like(X), 2, cfg.tau, cfg.beta)
     torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------- vector packing along x
+# Narrow meshes put several vectors side by side in one canonical tile row (KSplit::vp, DESIGN.md
+# §5.4): the seams need no gap because the band rows hold zeros outside the matrix.  The packed
+# launch must match the unpacked one to rounding (a different launch shape splits the z-columns
+# into different CTA ranges, so the partial planes are summed in a different order) and the oracle
+# to 1e-11, also for a batch that does not fill its last group.
+@pytest.mark.parametrize("n,batch,vpack", [(12, 7, 0), (24, 5, 3), (34, 9, 4), (18, 3, 2)])
+def test_vector_packing_apply(env, n, batch, vpack):
+    torch, igalr, workloads = env
+    cfg = synth.scaled(synth.CONFIGS["c2"], n, batch=batch)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    x = np.random.default_rng(n * 31 + batch).standard_normal((batch, n, n, n))
+    xd = torch.from_numpy(x).cuda()
+    outs = {}
+    for vp in (1, vpack):
+        op._test_knobs(vpack=vp)
+        ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+        op.apply(xd, ym, ys)
+        torch.cuda.synchronize()
+        outs[vp] = (ym.cpu().numpy(), ys.cpu().numpy())
+    op._test_knobs()
+    assert rel(outs[vpack][0], outs[1][0]) <= 1e-14 and rel(outs[vpack][1], outs[1][1]) <= 1e-14
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    for b in range(batch):
+        assert rel(outs[vpack][0][b], oracle.spmv(M, x[b])) <= TOL
+        assert rel(outs[vpack][1][b], oracle.spmv(S, x[b])) <= TOL
+
+
+@pytest.mark.parametrize("n,nt", [(12, 5), (22, 7)])
+def test_vector_packing_kkt(env, n, nt):
+    # the KKT's mass launch (3 n_t vectors) and batch-split stiffness launch (2 n_t vectors, the
+    # split inside a packed group) packed vs unpacked, and against the oracle's paper rows
+    torch, igalr, workloads = env
+    cfg = synth.scaled(synth.CONFIGS["c4"], n, n_t=nt)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    m = n - 2
+    X = np.random.default_rng(7 * n + nt).standard_normal((3, nt, m, m, m))
+    Xd = torch.from_numpy(X).cuda()
+    outs = []
+    for vp in (1, 0, 3):
+        op._test_knobs(vpack=vp)
+        out = torch.empty_like(Xd)
+        op.kkt_apply(Xd, out, nt, cfg.tau, cfg.beta)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    op._test_knobs()
+    assert rel(outs[1], outs[0]) <= 1e-14 and rel(outs[2], outs[0]) <= 1e-14
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    ref = oracle.kkt_apply_csr(M, S, X, cfg.tau, cfg.beta)
+    assert rel(outs[1], ref) <= TOL
+
+
+def test_vector_packing_chosen_for_c4(env):
+    # the tile choice packs the c4 mesh (46 interior columns: 184 of 192 columns with 4 vectors
+    # instead of 46 of 64) and keeps c3 (128 columns) and a single vector unpacked
+    torch, igalr, workloads = env
+    for name, batch, packed in (("c4", 64, True), ("c4", 1, False), ("c3", 8, False)):
+        cfg = synth.CONFIGS[name]
+        op = workloads.build_operator(cfg, synth.draw_weights(cfg))
+        qx, lw, vp = op._test_tile(batch)
+        assert (vp > 1) == packed, (name, batch, qx, lw, vp)
+        if packed:
+            assert (vp * 46) / (-(-vp * 46 // (32 * qx)) * 32 * qx) > 0.9
