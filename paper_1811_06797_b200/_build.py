@@ -38,17 +38,17 @@ GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]ELb[01]EEEv")
 _MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dELb%dEEEvNS0_5Args2ENS0_6KSplitE"
 KNOWN_SPILLS = {
     _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 0): (20, 40),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 1): (52, 72),
     _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 0): (12, 16),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 1): (32, 44),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 4, 0, 1): (44, 60),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 1): (20, 28),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 4, 0, 1): (20, 28),
     _MK % ("11ShapeStiffA", 3, 12, 2, 1, 0): (56, 76),
     _MK % ("11ShapeStiffA", 3, 16, 1, 0, 1): (4, 4),
+    _MK % ("11ShapeStiffA", 3, 16, 1, 1, 1): (52, 72),
     _MK % ("11ShapeStiffA", 3, 16, 2, 0, 1): (4, 4),
     _MK % ("11ShapeStiffA", 3, 16, 2, 1, 0): (44, 60),
-    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 1): (52, 72),
+    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 1): (44, 60),
     _MK % ("11ShapeStiffA", 3, 16, 4, 0, 1): (4, 4),
-    _MK % ("11ShapeStiffA", 3, 16, 4, 1, 1): (52, 72),
+    _MK % ("11ShapeStiffA", 3, 16, 4, 1, 1): (44, 60),
     _MK % ("10ShapeMassKILi3EE", 4, 12, 2, 0, 0): (64, 80),
     _MK % ("10ShapeMassKILi3EE", 4, 12, 4, 0, 0): (68, 88),
     _MK % ("10ShapeMassKILi4EE", 4, 12, 1, 0, 0): (32, 32),

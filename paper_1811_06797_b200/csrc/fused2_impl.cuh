@@ -100,6 +100,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 __device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0));
 }
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 // ---- mbarrier / TMA helpers
@@ -706,7 +709,8 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #endif
 #ifdef IGALR_EXP_TIMERS
     // experiment: per-warp cycle accounting of the round loop (sync, coefficient loads, sweep, retire)
-    long long exp_t[5] = {0, 0, 0, 0, 0}, exp_acc[4] = {0, 0, 0, 0};
+    long long exp_t[5] = {0, 0, 0, 0, 0}, exp_acc[4] = {0, 0, 0, 0}, exp_bar = 0, exp_pw = 0, exp_tb = 0, exp_tw = 0,
+              exp_sx = 0, exp_xw = 0, exp_sp = 0;
     const long long exp_t_start = clock64();
 #define EXP_T(k)                                                        \
     do {                                                                \
@@ -827,13 +831,35 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             if (threadIdx.x == 0) {
                 const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
                 int ncol = 0;
-                plane_pieces([&](int, int, int, int n) { ncol += n; });
+                if constexpr (!PACK) plane_pieces([&](int, int, int, int n) { ncol += n; });  // (PACK: cp.async rows)
                 const uint32_t rb = (uint32_t)(ncol * sizeof(double));
                 const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
                 mbar_expect_tx(&pbar[buf], (uint32_t)max(rhi - rlo, 0) * rb + zbytes);
             }
         };
         auto stage_plane = [&](int zp, int buf) {
+            if constexpr (GSYNC && PACK) {
+                // packed rows: up to ~3 pieces per row, too many bulk copies for the issuing lanes (each
+                // costs a uniform-register round trip): every thread copies 16-byte chunks with
+                // cp.async (completion: cp.async.wait_group before the plane's CTA barrier); the z
+                // record stays one bulk copy on pbar[buf]
+                const int cbase = x0 - P - PADL;
+                const int rlo = max(0, P - y0), rhi = min(HY, a.my - y0 + P);
+                plane_pieces([&](int v, int lx, int c, int n) {
+                    const double* srcp = a.src + vsrc(v) + (long long)zp * plane + lx + (long long)(y0 - P) * a.mx;
+                    double* dstp = vin + buf * VSZ + (c - cbase);
+                    for (int r = rlo + warp; r < rhi; r += NW * WPQ)
+                        for (int k = lane; 2 * k < n; k += 32)
+                            cp16(dstp + r * HXP + 2 * k, srcp + (long long)r * a.mx + 2 * k);
+                });
+                cp_commit();
+                if (threadIdx.x == 0) {
+                    stage_plane_expect(buf);
+                    const uint32_t zbytes = (uint32_t)(a.nrounds * NGB * sizeof(double));
+                    bulk_g2s(zcs + buf * a.nrounds * NGB, a.bz + (size_t)zp * a.nrounds * NGB, zbytes, &pbar[buf]);
+                }
+                return;
+            }
             if constexpr (GSYNC) {
                 // the in-range part of every tile row (widened to an even, 16-byte aligned column
                 // range) and the plane's z record, completing on pbar[buf].  Thread 0 registers the
@@ -941,7 +967,7 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
             copy_yrows(ycs + (size_t)buf * TY * YROW, R, y0);
         };
 
-        if constexpr (GSYNC && DIST) {
+        if constexpr (GSYNC && DIST && !PACK) {
             stage_plane_expect(0);
             __syncthreads();  // the expected byte count is registered before any copy completes
         }
@@ -955,20 +981,49 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 EXP_T(0);
                 if constexpr (GSYNC) {
                     tm_wait_st();
+#ifdef IGALR_EXP_TIMERS
+                    exp_tw += clock64() - exp_t[0];
+#endif
                     if (r == 0) {  // new plane buffer: CTA barrier, then request plane z'+1
                         cp_wait<0>();  // (resident y-coefficients at a segment start)
-                        if (DIST && zp + 1 < zb) stage_plane_expect(pbuf ^ 1);
+                        if (DIST && !PACK && zp + 1 < zb) stage_plane_expect(pbuf ^ 1);
+#ifdef IGALR_EXP_TIMERS
+                        exp_tb = clock64();
+#endif
                         __syncthreads();
+#ifdef IGALR_EXP_TIMERS
+                        exp_bar += clock64() - exp_tb;
+#endif
+#ifdef IGALR_EXP_TIMERS
+                        exp_tb = clock64();
+#endif
                         if (zp + 1 < zb) stage_plane(zp + 1, pbuf ^ 1);
+#ifdef IGALR_EXP_TIMERS
+                        exp_sp += clock64() - exp_tb;
+                        exp_tb = clock64();
+#endif
                         mbar_wait(&pbar[pbuf], (pph >> pbuf) & 1);
+#ifdef IGALR_EXP_TIMERS
+                        exp_pw += clock64() - exp_tb;
+#endif
                         pph ^= 1u << pbuf;
                     } else {
                         asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(GTHREADS) : "memory");
                     }
                     // the group is past round r-1: its x buffer can take round r+1
+#ifdef IGALR_EXP_TIMERS
+                    exp_tb = clock64();
+#endif
                     if (!last_round) stage_xc(r + 1, xbuf ^ 1);
                     else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+#ifdef IGALR_EXP_TIMERS
+                    exp_sx += clock64() - exp_tb;
+                    exp_tb = clock64();
+#endif
                     mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
+#ifdef IGALR_EXP_TIMERS
+                    exp_xw += clock64() - exp_tb;
+#endif
                     xph ^= 1u << xbuf;
                     EXP_T(1);
                 } else {
@@ -1290,8 +1345,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #endif
 #ifdef IGALR_EXP_TIMERS
     if (lane == 0 && (blockIdx.x % 37) == 0)
-        printf("EXPT cta %d warp %d total %lld sync %lld load %lld sweep %lld retire %lld\n", blockIdx.x, warp,
-               clock64() - exp_t_start, exp_acc[0], exp_acc[1], exp_acc[2], exp_acc[3]);
+        printf("EXPT cta %d warp %d total %lld sync %lld load %lld sweep %lld retire %lld bar %lld pwait %lld tmw %lld "
+               "splane %lld sxc %lld xwait %lld\n",
+               blockIdx.x, warp, clock64() - exp_t_start, exp_acc[0], exp_acc[1], exp_acc[2], exp_acc[3], exp_bar, exp_pw,
+               exp_tw, exp_sp, exp_sx, exp_xw);
 #endif
 #undef EXP_T
     asm volatile("tcgen05.fence::before_thread_sync;");
