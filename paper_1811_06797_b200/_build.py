@@ -37,15 +37,15 @@ GUARDED = re.compile(r"k_canon.*ELb1ELb1ELb[01]ELb[01]EEEv")
 # c4 (P 3, LW 12, QX 2, split / packed) nothing; c5 stiffness and mass (P 4, LW 13, QX 4) nothing.
 _MK = "_ZN5igalr2f27k_canonINS0_%sELi%dELi%dELi2ELi%dELb1ELb1ELb%dELb%dEEEvNS0_5Args2ENS0_6KSplitE"
 KNOWN_SPILLS = {
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 0): (20, 40),
-    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 0): (12, 16),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 1, 0, 0): (20, 28),
+    _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 0): (16, 20),
     _MK % ("10ShapeMassKILi4EE", 3, 16, 2, 0, 1): (20, 28),
     _MK % ("10ShapeMassKILi4EE", 3, 16, 4, 0, 1): (20, 28),
-    _MK % ("11ShapeStiffA", 3, 12, 2, 1, 0): (56, 76),
+    _MK % ("11ShapeStiffA", 3, 12, 2, 1, 0): (52, 72),
     _MK % ("11ShapeStiffA", 3, 16, 1, 0, 1): (4, 4),
     _MK % ("11ShapeStiffA", 3, 16, 1, 1, 1): (52, 72),
     _MK % ("11ShapeStiffA", 3, 16, 2, 0, 1): (4, 4),
-    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 0): (44, 60),
+    _MK % ("11ShapeStiffA", 3, 16, 2, 1, 0): (60, 80),
     _MK % ("11ShapeStiffA", 3, 16, 2, 1, 1): (44, 60),
     _MK % ("11ShapeStiffA", 3, 16, 4, 0, 1): (4, 4),
     _MK % ("11ShapeStiffA", 3, 16, 4, 1, 1): (44, 60),

@@ -509,6 +509,7 @@ void iga_lr_destroy(iga_lr_op* op) {
         if (op->plan[k].d_f2) cudaFree(op->plan[k].d_f2);
         if (op->plan[k].d_canon) cudaFree(op->plan[k].d_canon);
         if (op->plan[k].d_ztab) cudaFree(op->plan[k].d_ztab);
+        if (op->plan[k].d_xtab) cudaFree(op->plan[k].d_xtab);
     }
     if (op->side) cudaStreamDestroy(op->side);
     if (op->host_sh) cudaStreamDestroy(op->host_sh);

@@ -64,7 +64,8 @@ struct Args2 {
     double scale;
     int accumulate;
     double* scratch;       // [nctas][NSEG][4P][L][TX] partial planes
-    const double* bx;
+    const double* bx;      // x-factor bands; on the unpacked GSYNC path instead the per-round x records
+                           // [nrounds][ceil(mx/32)][NX][32][BW] (k_build_xtab)
     const double* by;
     const double* bz;      // z-factor bands; on the GSYNC canonical path instead the per-plane z
                            // records [mz][nrounds][NGB] (slot-permuted, group-scaled; k_build_ztab)
@@ -697,6 +698,10 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
     // the group's x-coefficients, so rounds are separated by a group barrier (named barrier
     // 1 + grp) and only the first round of a plane (new plane buffer) by a CTA barrier.
     constexpr bool GSYNC = gsync_path<P, TMA, YRES>();
+    // XREC: one bulk copy per column group and round from the per-round x records (Args2::bx) instead
+    // of NX band-row copies: the producer's copy issue is a uniform-register round trip per copy
+    // (c3 -1.0 %).  p = 3 only: at p = 4 the change moves the mass kernel into spills (c5 +1 %)
+    constexpr bool XREC = GSYNC && !PACK && P == 3;
     // GSYNC plane staging: lane 0 of every warp issues a share of the row copies (DIST) or
     // thread 0 issues all of them
     constexpr bool DIST = !(P == 3 && QX == 4);
@@ -925,8 +930,14 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 // the column group's 32 columns of every x-entry
                 if (gprod) {
                     mbar_expect_tx(&xbar[grp][buf], (uint32_t)(NX * TXW * BW * sizeof(double)));
-                    // packed columns [c0, c0 + 32) in pieces of one vector each (the band rows of the
-                    // local columns; columns past the packed width read the last vector's padding rows)
+                    if constexpr (XREC) {
+                        // the group's x record of round r: one copy of NX x 32 band rows, laid out
+                        // [NX][32][BW] at the group's slot of the buffer (k_build_xtab)
+                        const int nblk = (a.mx + TXW - 1) / TXW;
+                        bulk_g2s(dstp + grp * NX * TXW * BW, a.bx + ((size_t)r * nblk + x0 / TXW + grp) * NX * TXW * BW,
+                                 (uint32_t)(NX * TXW * BW * sizeof(double)), &xbar[grp][buf]);
+                        return;
+                    }
                     if constexpr (!PACK) {
 #pragma unroll
                         for (int e = 0; e < NX; ++e)
@@ -935,6 +946,8 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                                      (uint32_t)(TXW * BW * sizeof(double)), &xbar[grp][buf]);
                         return;
                     }
+                    // packed columns [c0, c0 + 32) in pieces of one vector each (the band rows of the
+                    // local columns; columns past the packed width read the last vector's padding rows)
                     const int c0 = x0 + grp * TXW;
                     for (int c = c0; c < c0 + TXW;) {
                         const int vi = min(c / a.mx, VPK - 1);
@@ -1049,7 +1062,9 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #pragma unroll
                 for (int e = 0; e < NX; ++e)
 #pragma unroll
-                    for (int k = 0; k < BW; ++k) xr[e][k] = xc[(e * TX + cx) * BW + k];
+                    for (int k = 0; k < BW; ++k)
+                        xr[e][k] = XREC ? xc[((grp * NX + e) * TXW + lane) * BW + k]  // (x-record layout)
+                                        : xc[(e * TX + cx) * BW + k];
                 // p = 4 stiffness on the GSYNC path reads the (pre-scaled) z record from shared
                 // memory in the Z stage (broadcast loads) instead of holding NG x BW doubles in
                 // registers: its sweep sits at the 255-register cliff.  The freed registers take the
@@ -1917,6 +1932,7 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     a.bz = op->F[2].band;
     a.rounds = pl.d_canon;
     if (gsync_path<P, TMA, YRES>()) a.bz = pl.d_ztab;  // GSYNC path: per-plane z records
+    if (gsync_path<P, TMA, YRES>() && !PACK && P == 3) a.bx = pl.d_xtab;  // ... and per-round x records (XREC)
     a.nrounds = pl.canon_nrounds;
     a.mx = op->m[0];
     a.my = op->m[1];
@@ -2116,6 +2132,23 @@ __global__ void k_build_ztab(const double* __restrict__ bz, const int* __restric
     ztab[i] = v;
 }
 
+// Per-round x records of the unpacked GSYNC canonical kernel (one bulk copy per column group and
+// round): xtab[r][b][e][c][k] = Fx_{xf_r[e]}[32 b + c][k] (band entry k of row 32 b + c), 0 past mx.
+__global__ void k_build_xtab(const double* __restrict__ bx, const int* __restrict__ xf, int nrounds, int nx, int mx,
+                             int BW, double* __restrict__ xtab) {
+    const int nblk = (mx + 31) / 32;
+    const long long n = (long long)nrounds * nblk * nx * 32 * BW;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int k = (int)(i % BW);
+    const int c = (int)((i / BW) % 32);
+    const int e = (int)((i / (32LL * BW)) % nx);
+    const int b = (int)((i / (32LL * BW * nx)) % nblk);
+    const int r = (int)(i / (32LL * BW * nx * nblk));
+    const int col = b * 32 + c;
+    xtab[i] = col < mx ? bx[((size_t)xf[r * nx + e] * mx + col) * BW + k] : 0.0;
+}
+
 template <class S>
 iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl, cudaStream_t st) {
     std::vector<f2::RoundC<S>> v;
@@ -2138,8 +2171,21 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl, cudaStream_t st) {
         }
     int* d_gf = nullptr;
     double* d_gs = nullptr;
+    int* d_xf = nullptr;
+    std::vector<int> xf(n * S::NX);
+    for (int r = 0; r < n; ++r)
+        for (int x = 0; x < S::NX; ++x) xf[r * S::NX + x] = v[r].xf[x];
+    const int BWx = 2 * op->p[0] + 1, mx = op->m[0];
+    const size_t nxt = (size_t)n * ((mx + 31) / 32) * S::NX * 32 * BWx;
     const size_t nz = (size_t)mz * n * ngb;
     e = cudaMalloc(&pl->d_ztab, sizeof(double) * nz);
+    if (!e) e = cudaMalloc(&pl->d_xtab, sizeof(double) * nxt);
+    if (!e) e = pool_alloc(op->pool, (void**)&d_xf, sizeof(int) * xf.size(), st);
+    if (!e) e = cudaMemcpyAsync(d_xf, xf.data(), sizeof(int) * xf.size(), cudaMemcpyHostToDevice, st);
+    if (!e) {
+        k_build_xtab<<<(unsigned)((nxt + 255) / 256), 256, 0, st>>>(op->F[0].band, d_xf, n, S::NX, mx, BWx, pl->d_xtab);
+        e = cudaGetLastError();
+    }
     if (!e) e = pool_alloc(op->pool, (void**)&d_gf, sizeof(int) * gf.size(), st);
     if (!e) e = pool_alloc(op->pool, (void**)&d_gs, sizeof(double) * gs.size(), st);
     if (!e) e = cudaMemcpyAsync(d_gf, gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice, st);
@@ -2153,6 +2199,7 @@ iga_status prepare_canon_t(const iga_lr_op* op, Plan* pl, cudaStream_t st) {
     // here, so wait for this stream
     if (d_gf) cudaFreeAsync(d_gf, st);
     if (d_gs) cudaFreeAsync(d_gs, st);
+    if (d_xf) cudaFreeAsync(d_xf, st);
     if (!e) e = cudaStreamSynchronize(st);
     if (e) return cuda_error(e, "canon z records");
     pl->canon_nrounds = n;

@@ -82,6 +82,7 @@ struct Plan {
     bool f2_ok = false;
     void* d_canon = nullptr;        // canonical-shape round tables (apply_fused2.cu)
     double* d_ztab = nullptr;       // per-plane z records of the canonical kernel (GSYNC path)
+    double* d_xtab = nullptr;       // per-round x records [round][32-column block][NX][32][BW] (GSYNC)
     int canon_nrounds = 0;
     bool canon_ok = false;
     int canon_mk = 4;               // mass terms per sweep of the canonical mass shape

@@ -38,6 +38,9 @@ def main(rep, title):
         for k, name in KEYS:
             if k in d:
                 print("| %s | %s %s |" % (name, d[k], u.get(k, "")))
+        for k in hdr:  # FP64 tensor-core (DMMA) pipe counters, where the report has them
+            if "dmma" in k and (k.endswith("pct_of_peak_sustained_active") or k.endswith(".sum")):
+                print("| %s | %s %s |" % (k, d[k], u.get(k, "")))
         print("\nStall reasons (warp cycles per issued instruction):\n")
         print("| stall | per issue |\n|---|---|")
         for s in STALLS:
