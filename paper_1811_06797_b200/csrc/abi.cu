@@ -687,33 +687,42 @@ iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double be
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = (int64_t)op->m[0] * op->m[1] * op->m[2];
     const size_t blk = (size_t)n_t * N;
+    const bool sym = op->stiff_sym;
+    const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
+                       (sym || op->plan[kPlanF2StiffT].canon_ok) && !op->knobs.force_generic;
+    if (canon) {
+        // Canonical route (kkt.cu, k_kkt_combine): T = [M y, M u, M lambda, tau S^T lambda, tau S y], then
+        // the per-step combinations.  One mass launch over the 3 n_t input vectors and one stiffness
+        // launch over 2 n_t vectors ([lambda, y]: a batch split, vectors n_t.. read y at `in`), neither
+        // accumulating: no launch reads its own output back.
+        double* T = nullptr;
+        cudaError_t e = pool_alloc(op->pool, (void**)&T, sizeof(double) * 5 * blk, st);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
+        iga_status s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, in, T, 1.0, 0, 3 * n_t, st);
+        if (!s && !sym) {
+            // K != K^T: the lambda block takes the K^T plans
+            s = apply_canon_part(op, op->plan[kPlanF2StiffT], 1, in + 2 * blk, T + 3 * blk, tau, 0, n_t, st);
+            if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, T + 4 * blk, tau, 0, n_t, st);
+        } else if (!s) {
+            CanonSplit sp;
+            sp.bsplit = n_t;
+            sp.src_jump = -3 * (long long)blk;  // in + 2 blk + b N - 3 blk = in + (b - n_t) N
+            sp.dst_jump = 0;                    // T + 3 blk + b N = T + 4 blk + (b - n_t) N
+            s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, T + 3 * blk, tau, 0, 2 * n_t, st, sp);
+            if (s == IGA_EUNSUPPORTED) {  // no split variant for this shape: one launch per segment
+                s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, T + 3 * blk, tau, 0, n_t, st);
+                if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, T + 4 * blk, tau, 0, n_t, st);
+            }
+        }
+        if (!s) s = kkt_combine(T, out, n_t, N, tau, beta, st);
+        cudaFreeAsync(T, st);
+        return s;
+    }
     double* abc = nullptr;  // a, b, c combos [3][n_t][N]
     cudaError_t e = pool_alloc(op->pool, (void**)&abc, sizeof(double) * 3 * blk, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync(kkt)");
     iga_status s = kkt_combos(in, abc, n_t, N, tau, beta, st);  // abc = [b, tau a, c]
-    const bool sym = op->stiff_sym;
-    const bool canon = want_f2(op, 3 * n_t, flags) && op->plan[kPlanF2Mass].canon_ok && op->plan[kPlanF2Stiff].canon_ok &&
-                       (sym || op->plan[kPlanF2StiffT].canon_ok) && !op->knobs.force_generic;
-    if (!s && canon && !sym) {
-        // K != K^T: r_y += tau K^T lambda and r_lam += tau K y are two accumulating launches
-        s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
-        if (!s) s = apply_canon_part(op, op->plan[kPlanF2StiffT], 1, in + 2 * blk, out, tau, 1, n_t, st);
-        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
-    } else if (!s && canon) {
-        // (r_y, r_u, r_lam) = M [b, tau a, c] in one launch over 3 n_t vectors, then one
-        // accumulating stiffness launch over 2 n_t vectors: [lambda, y] -> [r_y, r_lam] (a batch
-        // split: vectors n_t.. read y at in and write r_lam at out + 2 blk)
-        s = apply_canon_part(op, op->plan[kPlanF2Mass], 0, abc, out, 1.0, 0, 3 * n_t, st);
-        CanonSplit sp;
-        sp.bsplit = n_t;
-        sp.src_jump = -3 * (long long)blk;  // in + 2 blk + b N - 3 blk = in + (b - n_t) N
-        sp.dst_jump = (long long)blk;       // out + b N + blk = out + 2 blk + (b - n_t) N
-        if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, 2 * n_t, st, sp);
-        if (s == IGA_EUNSUPPORTED) {  // no split variant for this shape: one launch per segment
-            s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in + 2 * blk, out, tau, 1, n_t, st);
-            if (!s) s = apply_canon_part(op, op->plan[kPlanF2Stiff], 1, in, out + 2 * blk, tau, 1, n_t, st);
-        }
-    } else if (!s) {
+    if (!s) {
         // r_y = M b + tau S^T lambda ; r_u = tau M a ; r_lambda = M c + tau S y
         s = apply2_impl(op, abc, in + 2 * blk, out, 1.0, tau, n_t, flags, stream, !sym);
         if (!s) s = iga_lr_apply2(op, abc + blk, nullptr, out + blk, 1.0, 0.0, n_t, flags, stream);

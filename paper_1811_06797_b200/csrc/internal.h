@@ -205,5 +205,6 @@ iga_status kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, 
 bool kkt_prec_matches(const iga_kkt_prec* P, const iga_lr_op* op, int n_t, double tau, double beta);
 iga_status kkt_combos(const double* in, double* abc, int n_t, int64_t N, double tau, double beta,
                       cudaStream_t st);
+iga_status kkt_combine(const double* T, double* out, int n_t, int64_t N, double tau, double beta, cudaStream_t st);
 
 }  // namespace igalr
