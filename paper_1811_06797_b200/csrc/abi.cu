@@ -320,6 +320,7 @@ iga_status iga_quad_nodes(const iga_space* sp, int32_t dir, double* nodes_out, i
 
 iga_status iga_lr_assemble_factors(const iga_space* sp, const iga_sep* omega, const iga_sep* const* q, uint32_t flags,
                                    void* stream, iga_lr_op** out) {
+    NvtxRange nvtx_("iga_lr_assemble_factors");
     g_err.clear();
     if (!out) return set_error(IGA_EINVAL, "out is NULL");
     *out = nullptr;
@@ -639,12 +640,14 @@ static iga_status apply2_impl(const iga_lr_op* op, const double* x_mass, const d
 
 iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double* x_stiff, double* out, double alpha,
                          double gamma, int32_t batch, uint32_t flags, void* stream) {
+    NvtxRange nvtx_("iga_lr_apply2");
     g_err.clear();
     return apply2_impl(op, x_mass, x_stiff, out, alpha, gamma, batch, flags, stream, false);
 }
 
 iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, double* y_stiff, double alpha,
                         double gamma, int32_t batch, uint32_t flags, void* stream) {
+    NvtxRange nvtx_("iga_lr_apply");
     g_err.clear();
     if (!op) return set_error(IGA_EINVAL, "op is NULL");
     if (!x) return set_error(IGA_EINVAL, "x is NULL");
@@ -675,6 +678,7 @@ iga_status iga_lr_apply(const iga_lr_op* op, const double* x, double* y_mass, do
 
 iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in, double* out,
                          uint32_t flags, void* stream) {
+    NvtxRange nvtx_("iga_kkt_apply");
     g_err.clear();
     if (!op) return set_error(IGA_EINVAL, "op is NULL");
     if (!op->has_mass || !op->has_stiff) return set_error(IGA_ESTATE, "KKT needs mass and stiffness");
@@ -750,6 +754,7 @@ static iga_status host_roundtrip(const iga_lr_op* op, size_t in_elems, size_t ou
 // kernels.  Device buffers are stream-ordered scratch on the caller's stream.
 iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* y_mass_host, double* y_stiff_host,
                              double alpha, double gamma, int32_t batch, uint32_t flags, void* stream) {
+    NvtxRange nvtx_("iga_lr_apply_host");
     g_err.clear();
     if (!op || !x_host || batch < 1 || (!y_mass_host && !y_stiff_host)) return set_error(IGA_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
@@ -834,6 +839,7 @@ iga_status iga_lr_apply_host(const iga_lr_op* op, const double* x_host, double* 
 
 iga_status iga_kkt_apply_host(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in_host,
                               double* out_host, uint32_t flags, void* stream) {
+    NvtxRange nvtx_("iga_kkt_apply_host");
     g_err.clear();
     if (!op || !in_host || !out_host || n_t < 1) return set_error(IGA_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;

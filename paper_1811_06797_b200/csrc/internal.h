@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; a no-op stub unless a profiler injects itself
 
 #include <mutex>
 #include <string>
@@ -11,6 +12,15 @@
 #include "iga_lr.h"
 
 namespace igalr {
+
+// NVTX range over one C-ABI call (timeline annotation for nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 constexpr int kMaxP = 6;        // compiled degree range 1..kMaxP
 constexpr int kMaxNq = 16;      // Gauss points per span

@@ -160,6 +160,7 @@ using namespace igalr;
 extern "C" iga_status iga_kkt_minres(const iga_lr_op* op, const iga_kkt_prec* prec, int32_t n_t, double tau,
                                      double beta, const double* rhs, double* x, double rtol, int32_t maxit,
                                      uint32_t flags, void* stream, iga_minres_info* info) {
+    NvtxRange nvtx_("iga_kkt_minres");
     clear_error();
     if (!op) return set_error(IGA_EINVAL, "op is NULL");
     if (!rhs || !x) return set_error(IGA_EINVAL, "NULL rhs/x");

@@ -394,6 +394,7 @@ using namespace igalr;
 
 extern "C" iga_status iga_kkt_prec_create(const iga_lr_op* op, int32_t n_t, double tau, double beta, uint32_t flags,
                                           void* stream, iga_kkt_prec** out) {
+    NvtxRange nvtx_("iga_kkt_prec_create");
     clear_error();
     if (!op || !out) return set_error(IGA_EINVAL, "NULL op/out");
     *out = nullptr;
@@ -529,6 +530,7 @@ extern "C" void iga_kkt_prec_destroy(iga_kkt_prec* P) {
 }
 
 extern "C" iga_status iga_kkt_prec_apply(const iga_kkt_prec* P, const double* in, double* out, void* stream) {
+    NvtxRange nvtx_("iga_kkt_prec_apply");
     clear_error();
     if (!P || !in || !out) return set_error(IGA_EINVAL, "NULL argument");
     if (in == out) return set_error(IGA_EINVAL, "in and out alias");

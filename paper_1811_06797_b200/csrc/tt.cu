@@ -207,6 +207,7 @@ iga_status iga_lr_terms(const iga_lr_op* op, int32_t part, int32_t* n_terms, int
 
 iga_status iga_tt_kron_apply(const iga_lr_op* op, int32_t part, int32_t R1, int32_t R2, const double* gz,
                              const double* gy, const double* gx, double* wz, double* wy, double* wx, void* stream) {
+    NvtxRange nvtx_("iga_tt_kron_apply");
     if (iga_status s = check_op(op, part)) return s;
     if (R1 < 1 || R2 < 1) return set_error(IGA_EINVAL, "TT ranks must be >= 1");
     if (!gz || !gy || !gx || !wz || !wy || !wx) return set_error(IGA_EINVAL, "NULL core pointer");
@@ -225,6 +226,7 @@ iga_status iga_tt_kron_apply(const iga_lr_op* op, int32_t part, int32_t R1, int3
 iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, int32_t R1, int32_t R2,
                              const double* gz, const double* gy, const double* gx, double* L, double* R,
                              void* stream) {
+    NvtxRange nvtx_("iga_tt_interfaces");
     if (iga_status s = check_op(op, part)) return s;
     if (R1 < 1 || R2 < 1) return set_error(IGA_EINVAL, "TT ranks must be >= 1");
     if (site < 0 || site > 2) return set_error(IGA_EINVAL, "site must be 0 (x), 1 (y) or 2 (z)");
@@ -294,6 +296,7 @@ iga_status iga_tt_interfaces(const iga_lr_op* op, int32_t part, int32_t site, in
 
 iga_status iga_tt_local_apply(const iga_lr_op* op, int32_t part, int32_t site, int32_t Rl, int32_t Rr,
                               const double* L, const double* R, const double* x, double* y, void* stream) {
+    NvtxRange nvtx_("iga_tt_local_apply");
     if (iga_status s = check_op(op, part)) return s;
     if (Rl < 1 || Rr < 1) return set_error(IGA_EINVAL, "ranks must be >= 1");
     if (site < 0 || site > 2) return set_error(IGA_EINVAL, "site must be 0 (x), 1 (y) or 2 (z)");
