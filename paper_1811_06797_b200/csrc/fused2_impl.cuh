@@ -988,6 +988,14 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
         stage_xc(0, 0);
         cp_commit();
         int pbuf = 0, xbuf = 0;
+        // single-round plans (R <= 4 mass): every plane of the segment uses the same x-coefficients, so
+        // they are staged and loaded into registers once per segment (GSYNC path)
+        // (the packed 64-wide p = 3 mass kernel only, c4's: the stiffness kernels have more than one round
+        // for every R > 1, and the other mass variants spill 40-200 B when the registers live that long;
+        // they keep the per-round array)
+        constexpr bool XONCE = GSYNC && !std::is_same<S, ShapeStiffA>::value && P == 3 && QX == 2 && PACK;
+        const bool xonce = XONCE && a.nrounds == 1;
+        double xr_seg[XONCE ? NX : 1][XONCE ? BW : 1];
         for (int zp = za; zp < zb; ++zp) {
             for (int r = 0; r < a.nrounds; ++r) {
                 const bool last_round = (r == a.nrounds - 1);
@@ -1027,17 +1035,27 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
 #ifdef IGALR_EXP_TIMERS
                     exp_tb = clock64();
 #endif
-                    if (!last_round) stage_xc(r + 1, xbuf ^ 1);
-                    else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                    if constexpr (!XONCE) {
+                        if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                        else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                    } else if (!xonce) {
+                        if (!last_round) stage_xc(r + 1, xbuf ^ 1);
+                        else if (zp + 1 < zb) stage_xc(0, xbuf ^ 1);
+                    }
 #ifdef IGALR_EXP_TIMERS
                     exp_sx += clock64() - exp_tb;
                     exp_tb = clock64();
 #endif
-                    mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
+                    if constexpr (!XONCE) {
+                        mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
+                        xph ^= 1u << xbuf;
+                    } else if (!xonce || zp == za) {
+                        mbar_wait(&xbar[grp][xbuf], (xph >> xbuf) & 1);
+                        xph ^= 1u << xbuf;
+                    }
 #ifdef IGALR_EXP_TIMERS
                     exp_xw += clock64() - exp_tb;
 #endif
-                    xph ^= 1u << xbuf;
                     EXP_T(1);
                 } else {
                     if constexpr (TMA) {  // x-coefficients arrive by cp.async.bulk (mbarrier)
@@ -1059,12 +1077,26 @@ __global__ void __launch_bounds__(NW * WPQ * 32, 1) k_canon(const Args2 a, const
                 const double* yc = ycs + (size_t)(YRES ? r : xbuf) * TY * YROW + (size_t)row0 * YROW;
                 const double* zc = zcs + pbuf * a.nrounds * NGB + r * NGB;
                 double xr[NX][BW];
+                if constexpr (XONCE) {
+                    if (!xonce || zp == za) {
 #pragma unroll
-                for (int e = 0; e < NX; ++e)
+                        for (int e = 0; e < NX; ++e)
 #pragma unroll
-                    for (int k = 0; k < BW; ++k)
-                        xr[e][k] = XREC ? xc[((grp * NX + e) * TXW + lane) * BW + k]  // (x-record layout)
-                                        : xc[(e * TX + cx) * BW + k];
+                            for (int k = 0; k < BW; ++k)
+                                xr_seg[e][k] = XREC ? xc[((grp * NX + e) * TXW + lane) * BW + k] : xc[(e * TX + cx) * BW + k];
+                    }
+#pragma unroll
+                    for (int e = 0; e < NX; ++e)
+#pragma unroll
+                        for (int k = 0; k < BW; ++k) xr[e][k] = xr_seg[e][k];
+                } else {
+#pragma unroll
+                    for (int e = 0; e < NX; ++e)
+#pragma unroll
+                        for (int k = 0; k < BW; ++k)
+                            xr[e][k] = XREC ? xc[((grp * NX + e) * TXW + lane) * BW + k]  // (x-record layout)
+                                            : xc[(e * TX + cx) * BW + k];
+                }
                 // p = 4 stiffness on the GSYNC path reads the (pre-scaled) z record from shared
                 // memory in the Z stage (broadcast loads) instead of holding NG x BW doubles in
                 // registers: its sweep sits at the 255-register cliff.  The freed registers take the
