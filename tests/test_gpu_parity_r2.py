@@ -372,3 +372,31 @@ def test_vector_packing_chosen_for_c4(env):
         assert (vp > 1) == packed, (name, batch, qx, lw, vp)
         if packed:
             assert (vp * 46) / (-(-vp * 46 // (32 * qx)) * 32 * qx) > 0.9
+
+
+# ----------------------------------------------------------------- whole-tile CTA ranges
+# A canonical launch whose tiles number 90-100 % of the SMs gives every CTA one whole tile (no partial
+# planes, no fixup launch).  140 one-tile vectors on a 148-SM GPU take that route (and
+# 100 do not): both must match the oracle, and the vectors they share must agree to rounding.
+def test_whole_tile_cta_ranges(env):
+    torch, igalr, workloads = env
+    n = 12
+    cfg = synth.scaled(synth.CONFIGS["c2"], n, batch=140)
+    w = synth.draw_weights(cfg)
+    op = workloads.build_operator(cfg, w)
+    op._test_knobs(vpack=1)  # one vector per tile row: tiles = batch
+    x = np.random.default_rng(5).standard_normal((140, n, n, n))
+    xd = torch.from_numpy(x).cuda()
+    ym, ys = torch.empty_like(xd), torch.empty_like(xd)
+    op.apply(xd, ym, ys)
+    ym2, ys2 = torch.empty_like(xd[:100]), torch.empty_like(xd[:100])
+    op.apply(xd[:100].contiguous(), ym2, ys2)
+    torch.cuda.synchronize()
+    op._test_knobs()
+    assert rel(ym[:100].cpu().numpy(), ym2.cpu().numpy()) <= 1e-14
+    assert rel(ys[:100].cpu().numpy(), ys2.cpu().numpy()) <= 1e-14
+    P = oracle.problem_from_config(cfg, w)
+    M, S = oracle.assemble_csr(P)
+    for b in (0, 57, 99, 100, 139):
+        assert rel(ym[b].cpu().numpy(), oracle.spmv(M, x[b])) <= TOL
+        assert rel(ys[b].cpu().numpy(), oracle.spmv(S, x[b])) <= TOL
