@@ -129,7 +129,10 @@ iga_status iga_lr_apply2(const iga_lr_op* op, const double* x_mass, const double
    calK^T carries S^T (PAPER.md:306 writes the y-row as lambda_k (M + tau K)): when the op was
    assembled with q[k*3+l] and q[l*3+k] that differ (in R, coefficients or tables), S is not
    symmetric and the op holds a second plan for S^T (block (k,l) of S^T = weight q_kl with the
-   derivative patterns of block (l,k)), so the KKT matrix stays symmetric for MINRES. */
+   derivative patterns of block (l,k)), so the KKT matrix stays symmetric for MINRES.
+   Workspace: stream-ordered scratch from the op's pool, 5 n_t vectors ([M y, M u, M lambda,
+   tau S^T lambda, tau S y]; the rows are combined per time step afterwards) on the canonical
+   route, 3 n_t vectors on the generic fallback; the call does not synchronise `stream`. */
 iga_status iga_kkt_apply(const iga_lr_op* op, int32_t n_t, double tau, double beta, const double* in,
                          double* out, uint32_t flags, void* stream);
 
