@@ -375,17 +375,17 @@ def test_vector_packing_chosen_for_c4(env):
 
 
 # ----------------------------------------------------------------- whole-tile CTA ranges
-# A canonical launch whose tiles number 90-100 % of the SMs gives every CTA one whole tile (no partial
-# planes, no fixup launch).  140 one-tile vectors on a 148-SM GPU take that route (and
+# A canonical launch whose tiles number 95-100 % of the SMs gives every CTA one whole tile (no partial
+# planes, no fixup launch).  144 one-tile vectors on a 148-SM GPU take that route (and
 # 100 do not): both must match the oracle, and the vectors they share must agree to rounding.
 def test_whole_tile_cta_ranges(env):
     torch, igalr, workloads = env
     n = 12
-    cfg = synth.scaled(synth.CONFIGS["c2"], n, batch=140)
+    cfg = synth.scaled(synth.CONFIGS["c2"], n, batch=144)
     w = synth.draw_weights(cfg)
     op = workloads.build_operator(cfg, w)
     op._test_knobs(vpack=1)  # one vector per tile row: tiles = batch
-    x = np.random.default_rng(5).standard_normal((140, n, n, n))
+    x = np.random.default_rng(5).standard_normal((144, n, n, n))
     xd = torch.from_numpy(x).cuda()
     ym, ys = torch.empty_like(xd), torch.empty_like(xd)
     op.apply(xd, ym, ys)
@@ -397,6 +397,6 @@ def test_whole_tile_cta_ranges(env):
     assert rel(ys[:100].cpu().numpy(), ys2.cpu().numpy()) <= 1e-14
     P = oracle.problem_from_config(cfg, w)
     M, S = oracle.assemble_csr(P)
-    for b in (0, 57, 99, 100, 139):
+    for b in (0, 57, 99, 100, 143):
         assert rel(ym[b].cpu().numpy(), oracle.spmv(M, x[b])) <= TOL
         assert rel(ys[b].cpu().numpy(), oracle.spmv(S, x[b])) <= TOL
