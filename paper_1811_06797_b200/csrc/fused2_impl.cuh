@@ -2063,12 +2063,13 @@ cudaError_t launch_canon_t(const iga_lr_op* op, const Plan& pl, const double* sr
     if (a.units / nct < minlen) nct = a.units / minlen;
     if (nct < 1) nct = 1;
     while ((a.units + nct - 1) / nct > 3LL * a.mz) nct += sms;
-    // a launch whose tiles nearly fill the GPU (95-100 % of the SMs) takes one whole tile per CTA
-    // instead: no range boundary inside a tile, so no partial planes, no scratch traffic and no fixup
-    // launch (c4 mass: 144 tiles on 148 SMs).  Below ~95 % the idle SMs cost more than the boundaries
-    // (which are worth 3-5 % of a launch).
+    // a launch whose tiles nearly fill the GPU takes one whole tile per CTA instead: no range boundary
+    // inside a tile, so no partial planes, no scratch traffic and no fixup launch (c4 mass: 144 tiles on
+    // 148 SMs).  Measured on 48^3 meshes (B200): the boundaries cost a mass launch 7-8 % and a stiffness
+    // launch 2-3 %, so whole tiles win from 92 % (mass) and 97 % (stiffness) SM fill.
     const long long ntiles = a.units / a.mz;
-    if (op->knobs.minlen == 0 && ntiles <= sms && ntiles * 100 >= (long long)sms * 95) nct = ntiles;
+    const int fill = std::is_same<S, f2::ShapeStiffA>::value ? 97 : 92;
+    if (op->knobs.minlen == 0 && ntiles <= sms && ntiles * 100 >= (long long)sms * fill) nct = ntiles;
     a.nctas = (int)nct;
     const size_t sm = smem_bytes_canon<S, P, LW, WPQ, QX, YRES>(a.nrounds);
     auto kern = k_canon<S, P, LW, WPQ, QX, YRES, TMA, SPLIT, PACK>;

@@ -375,7 +375,7 @@ def test_vector_packing_chosen_for_c4(env):
 
 
 # ----------------------------------------------------------------- whole-tile CTA ranges
-# A canonical launch whose tiles number 95-100 % of the SMs gives every CTA one whole tile (no partial
+# A canonical launch whose tiles nearly fill the SMs (>= 92 % mass, >= 97 % stiffness) gives every CTA one whole tile (no partial
 # planes, no fixup launch).  144 one-tile vectors on a 148-SM GPU take that route (and
 # 100 do not): both must match the oracle, and the vectors they share must agree to rounding.
 def test_whole_tile_cta_ranges(env):
